@@ -1,0 +1,247 @@
+"""Generate the golden fixtures under tests/golden/ by running the REFERENCE
+package itself (``/root/reference/pkg/src/dhsa``, pure NumPy) in this
+container.  The reference does not exist on the GPU box; the fixtures it
+produces are committed and the tests read only them.
+
+Run:  PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+Every fixture stores its inputs (or a seed + SHA-256 of the regenerated
+inputs for the larger shapes) and the reference's outputs:
+
+topk.npz      topk_row (masks.py:103-122) on 300 rows incl. forced ties and the
+              known-answer cases of tests/test_masks.py:92-99
+decode.npz    DecodeSession.step rows (masks.py:205-237), multi-step, random
+              ragged bounds, incl. integer-valued keys (exact fp64 scores)
+prefill.npz   prefill_mask rows (masks.py:143-150) + dense_attention outputs
+              (core.py:98-119) with those masks
+group.npz     group-shared decode rows: mask_from_chunk_scores over the
+              head-aggregated S_c (harness.py:288-306) on extend_for_decode
+              bounds, agg = max and mean, 4 heads sharing one key set (GQA)
+centroids.npz aggregate_rows (chunk_repr.py:57-68), bitwise
+c1.npz        the C1 demo shape (L=4096, 8 heads, d=64, block 64, top-k 16,
+              budget 1025): 3 decode steps per head, fp32-valued inputs,
+              rows stored as (start, count) ranges + attention outputs
+"""
+
+import hashlib
+import os
+import sys
+
+import numpy as np
+
+sys.dont_write_bytecode = True
+sys.path.insert(0, "/root/reference/pkg/src")
+
+from dhsa.chunk_repr import aggregate_rows, build_chunk_reps, chunk_similarity  # noqa: E402
+from dhsa.chunking import extend_for_decode, static_boundaries  # noqa: E402
+from dhsa.core import TokenSequence, dense_attention  # noqa: E402
+from dhsa.masks import DecodeSession, mask_from_chunk_scores, prefill_mask, topk_row  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def sha(*arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+def pack_rows(rows):
+    rows = [np.asarray(r, dtype=np.int64) for r in rows]
+    off = np.zeros(len(rows) + 1, dtype=np.int64)
+    off[1:] = np.cumsum([len(r) for r in rows])
+    return np.concatenate(rows) if rows else np.zeros(0, np.int64), off
+
+
+def rand_bounds(rng, length, max_cuts=4):
+    if length < 2:
+        return [0, length]
+    cuts = sorted(set(rng.integers(1, length, size=int(rng.integers(0, max_cuts + 1))).tolist()))
+    return [0] + cuts + [length]
+
+
+def gen_topk():
+    rng = np.random.default_rng(1001)
+    scores, rows, budgets, out = [], [], [], []
+    cases = [(np.zeros(8), 5, 3), (np.array([5.0, 4.0, 3.0, -10.0]), 3, 3),
+             (np.array([0.0, -0.0, 0.0, -0.0, 1.0]), 4, 3)]
+    for _ in range(300):
+        n = int(rng.integers(1, 40))
+        s = rng.standard_normal(n)
+        if rng.random() < 0.4:
+            s = np.round(s, 1)
+        cases.append((s, int(rng.integers(0, n)), int(rng.integers(1, n + 3))))
+    for s, r, b in cases:
+        scores.append(np.asarray(s, np.float64))
+        rows.append(r)
+        budgets.append(b)
+        out.append(topk_row(s, r, b))
+    so = np.zeros(len(scores) + 1, dtype=np.int64)
+    so[1:] = np.cumsum([len(s) for s in scores])
+    flat = np.concatenate(scores)
+    iv, io = pack_rows(out)
+    np.savez_compressed(os.path.join(OUT, "topk.npz"), scores=flat, score_off=so,
+                        rows=np.array(rows), budgets=np.array(budgets),
+                        idx=iv, idx_off=io)
+
+
+def gen_decode():
+    rng = np.random.default_rng(2002)
+    recs = []
+    for case in range(40):
+        dim = int(rng.choice([3, 4, 8, 16, 64]))
+        prompt = int(rng.integers(2, 90))
+        steps = int(rng.integers(1, 8))
+        total = prompt + steps
+        if case % 5 == 4:  # integer-valued: exact scores, tie-heavy
+            k = rng.integers(-2, 3, size=(total, dim)).astype(np.float64)
+            q = rng.integers(-2, 3, size=(total, dim)).astype(np.float64)
+        else:
+            k = rng.standard_normal((total, dim)).astype(np.float32).astype(np.float64)
+            q = rng.standard_normal((total, dim)).astype(np.float32).astype(np.float64)
+        if case % 3 == 0:
+            bounds = static_boundaries(prompt, int(rng.choice([1, 4, 8, 16])))
+        else:
+            bounds = rand_bounds(rng, prompt, 6)
+        budget = int(rng.integers(1, total + 2))
+        sess = DecodeSession(k[:prompt], bounds, budget)
+        rows = []
+        for t in range(prompt, total):
+            rows.append(sess.step(q[t], k[t]))
+        recs.append(dict(q=q, k=k, bounds=np.array(bounds), budget=budget,
+                         prompt=prompt, rows=rows,
+                         cached=np.asarray(sess.cached_chunk_keys)))
+    save_records("decode.npz", recs)
+
+
+def save_records(name, recs):
+    blob = {"n": np.array(len(recs))}
+    for i, r in enumerate(recs):
+        for key, val in r.items():
+            if key == "rows":
+                iv, io = pack_rows(val)
+                blob[f"{i}_rows"] = iv
+                blob[f"{i}_rows_off"] = io
+            else:
+                blob[f"{i}_{key}"] = np.asarray(val)
+    np.savez_compressed(os.path.join(OUT, name), **blob)
+
+
+def gen_prefill():
+    rng = np.random.default_rng(3003)
+    recs = []
+    for case in range(24):
+        L = int(rng.integers(1, 70))
+        dim = int(rng.choice([2, 5, 8, 16]))
+        q = rng.standard_normal((L, dim))
+        k = rng.standard_normal((L, dim))
+        v = rng.standard_normal((L, dim))
+        if case % 4 == 3:
+            q = np.round(q)
+            k = np.round(k)
+        bounds = static_boundaries(L, int(rng.choice([1, 3, 8]))) if case % 2 else rand_bounds(rng, L, 5)
+        budget = int(rng.integers(1, L + 3))
+        seq = TokenSequence(q, k, v)
+        mask = prefill_mask(seq, bounds, budget)
+        out = dense_attention(seq, mask)
+        recs.append(dict(q=q, k=k, v=v, bounds=np.array(bounds), budget=budget,
+                         rows=list(mask.rows), out=out))
+    save_records("prefill.npz", recs)
+
+
+def gen_group():
+    rng = np.random.default_rng(4004)
+    recs = []
+    for case in range(24):
+        G = 4
+        dim = int(rng.choice([4, 8, 32]))
+        prompt = int(rng.integers(4, 80))
+        gen = int(rng.integers(0, 6))
+        total = prompt + gen + 1
+        k = rng.standard_normal((total, dim)).astype(np.float32).astype(np.float64)
+        qh = rng.standard_normal((G, total, dim)).astype(np.float32).astype(np.float64)
+        if case % 6 == 5:
+            k = np.round(k)
+            qh = np.round(qh)
+        pb = static_boundaries(prompt, 8) if case % 2 else rand_bounds(rng, prompt, 5)
+        budget = int(rng.integers(1, total + 2))
+        full = extend_for_decode(pb, total)
+        out = {}
+        for agg in ("max", "mean"):
+            per_head = []
+            for h in range(G):
+                seq = TokenSequence(qh[h], k, k)
+                per_head.append(chunk_similarity(build_chunk_reps(seq, full)))
+            st = np.stack(per_head)
+            sc = st.max(axis=0) if agg == "max" else st.mean(axis=0)
+            out[agg] = mask_from_chunk_scores(sc, full, budget).rows[total - 1]
+        recs.append(dict(k=k, q=qh, prompt_bounds=np.array(pb), budget=budget,
+                         gen=gen, rows=[out["max"], out["mean"]]))
+    save_records("group.npz", recs)
+
+
+def gen_centroids():
+    rng = np.random.default_rng(5005)
+    recs = []
+    for case in range(12):
+        L = int(rng.integers(1, 300))
+        dim = int(rng.choice([4, 64, 128]))
+        m = rng.standard_normal((L, dim)).astype(np.float32).astype(np.float64)
+        bounds = static_boundaries(L, 64) if case % 2 else rand_bounds(rng, L, 8)
+        recs.append(dict(m=m, bounds=np.array(bounds), c=aggregate_rows(m, bounds)))
+    save_records("centroids.npz", recs)
+
+
+def c1_inputs(seed=7):
+    """C1 demo shape; regenerated identically by tests (numpy PCG64)."""
+    rng = np.random.default_rng(seed)
+    H, L, d, steps = 8, 4096, 64, 3
+    q = rng.standard_normal((H, L + steps, d), dtype=np.float32)
+    k = rng.standard_normal((H, L + steps, d), dtype=np.float32)
+    v = rng.standard_normal((H, L + steps, d), dtype=np.float32)
+    return q, k, v, H, L, d, steps
+
+
+def to_ranges(row, self_idx):
+    r = [int(x) for x in row if x != self_idx]
+    out = []
+    for x in r:
+        if out and out[-1][0] + out[-1][1] == x:
+            out[-1][1] += 1
+        else:
+            out.append([x, 1])
+    return np.array(out, dtype=np.int64).reshape(-1, 2)
+
+
+def gen_c1():
+    q, k, v, H, L, d, steps = c1_inputs()
+    budget = 16 * 64 + 1
+    bounds = static_boundaries(L, 64)
+    blob = {"sha": np.array(sha(q, k, v)), "budget": np.array(budget)}
+    outs = np.zeros((H, steps, d))
+    for h in range(H):
+        sess = DecodeSession(k[h, :L].astype(np.float64), bounds, budget)
+        for s in range(steps):
+            t = L + s
+            row = sess.step(q[h, t].astype(np.float64), k[h, t].astype(np.float64))
+            blob[f"r_{h}_{s}"] = to_ranges(row, t)
+            seq = TokenSequence(q[h, : t + 1].astype(np.float64), k[h, : t + 1].astype(np.float64),
+                                v[h, : t + 1].astype(np.float64))
+            # per-row body of dense_attention (core.py:115-118) on the row
+            kk = seq.keys[row]
+            sc = np.einsum("jd,d->j", kk, seq.queries[t]) * (1.0 / np.sqrt(d))
+            e = np.exp(sc - sc.max())
+            outs[h, s] = (e / e.sum()) @ seq.values[row]
+    blob["out"] = outs
+    np.savez_compressed(os.path.join(OUT, "c1.npz"), **blob)
+
+
+if __name__ == "__main__":
+    gen_topk()
+    gen_decode()
+    gen_prefill()
+    gen_group()
+    gen_centroids()
+    gen_c1()
+    print("golden fixtures written to", OUT)
