@@ -1,0 +1,159 @@
+/*
+ * dhsa_b200.h — C ABI of libdhsa_b200.so, the sm_100a (B200) implementation of
+ * the DHSA sparse-attention hot path:
+ *
+ *   centroids (sum/sqrt(n), fp64)  ->  query-centroid scores (fp64)  ->
+ *   token-budget Top-K as a chunk walk  ->  exact softmax attention over the
+ *   selected token ranges (online softmax, split-KV partial merge).
+ *
+ * The reference (/root/reference/pkg/src/dhsa) is a pure-NumPy package with no
+ * FFI; its operator surface is the Python API re-exported by
+ * dhsa/__init__.py:7-49.  Each entry point below names the reference function
+ * whose arithmetic it replaces.  The Python package paper_2510_24606_b200
+ * re-exposes the reference names and signatures on top of these calls
+ * (see INTEGRATION.md for the ctypes binding a maintainer would add).
+ *
+ * Conventions
+ *  - All pointers are caller-owned DEVICE pointers; nothing is allocated
+ *    inside (workspace sizes are queried with the *_workspace_size calls).
+ *  - "unit" u = one (sequence, kv-head) pair; units are laid out densely, so
+ *    q/o rows of unit u with group size G are rows u*G .. u*G+G-1 and the
+ *    K/V cache of unit u starts at cache + u*cache_unit_stride (elements).
+ *  - Every call is asynchronous on `stream` and returns 0 on success or a
+ *    negative DHSA_E* code; dhsa_last_error() returns a thread-local message.
+ *  - Functions are re-entrant; the library keeps no mutable global state.
+ */
+#ifndef DHSA_B200_H
+#define DHSA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* dhsa_stream_t; /* == cudaStream_t */
+
+enum dhsa_dtype { DHSA_F64 = 0, DHSA_F32 = 1, DHSA_BF16 = 2 };
+enum dhsa_agg { DHSA_AGG_NONE = 0, DHSA_AGG_MAX = 1, DHSA_AGG_MEAN = 2 };
+enum dhsa_status {
+  DHSA_OK = 0,
+  DHSA_EINVAL = -1,   /* bad argument (shape, dtype, budget, alignment) */
+  DHSA_ECUDA = -2,    /* CUDA launch / driver failure */
+  DHSA_ERANGE = -3,   /* capacity exceeded (tiles, chunks) */
+};
+
+/* Chunk layout of the PROMPT part of each unit.  Either an explicit boundary
+ * list per unit (bounds[u*bounds_stride + c], c = 0..nchunks[u], the
+ * reference's `bounds`, chunking.py:23-39), or, when bounds == NULL, the static
+ * grid [0, block, 2*block, ..., plen[u]] (chunking.py:42-54). */
+typedef struct {
+  const int32_t* bounds;   /* device [U][bounds_stride] or NULL */
+  int64_t bounds_stride;   /* 0 = one list shared by all units */
+  const int32_t* nchunks;  /* device [U] prompt chunk count (explicit mode) */
+  const int32_t* plen;     /* device [U] prompt length in tokens */
+  int32_t block;           /* static grid chunk size (bounds == NULL) */
+  int32_t max_chunks;      /* host upper bound on prompt chunks over units */
+} dhsa_layout;
+
+const char* dhsa_last_error(void);
+int dhsa_version(void);
+
+/* K1 — chunk centroids c_j = (sum_{t in chunk j} x_t, accumulated in token
+ * order in fp64) / sqrt(n_j).  Replaces chunk_repr.aggregate_rows
+ * (chunk_repr.py:57-68; sequential_sum :29-35, aggregate_chunk :38-54).
+ * Bit-exact with the reference for any input dtype.
+ * x: [U][x_unit_stride] rows of D elements (row stride D).
+ * out: [U][out_unit_stride] fp64, chunk c at out + u*out_unit_stride + c*D.
+ * normalize = 0 returns the raw sequential sums (the generated-chunk running
+ * sum of masks.py:197-199 / :235). */
+int dhsa_centroids(int dtype, const void* x, int64_t x_unit_stride, int D, int U,
+                   dhsa_layout layout, int normalize, double* out,
+                   int64_t out_unit_stride, dhsa_stream_t stream);
+
+/* K3 (+K2) — decode scores of Algorithm 2 (masks.py:153-173): for every unit u
+ * and chunk j of [prompt chunks | generated chunk (if gen_count[u] >= 1)],
+ * score = q . c_j in fp64 with no 1/sqrt(d) (masks.py:164-165,
+ * chunk_repr.py:97-103).  The generated-chunk centroid is
+ * gen_sum[u] / sqrt(gen_count[u]) (masks.py:161).  With agg = MAX / MEAN the
+ * G per-head rows of a unit are reduced (harness.py:288-306) into one row per
+ * unit; with agg = NONE one row per q-head is written.
+ * scores: [U or U*G][sc_stride] fp64, prompt chunk c at [c], the generated
+ * chunk at [nchunks(u)].
+ * State update folded in (masks.py:235-236 without the count): when k_new is
+ * non-NULL, gen_sum[u] += k_new[u] (fp64, after it was read) and, when the
+ * caches are non-NULL, k_new/v_new are appended at token plen[u]+gen_count[u]
+ * of the K/V cache.  gen_count itself is advanced by dhsa_decode_advance. */
+int dhsa_decode_score(int dtype, const void* q, const double* centroids,
+                      int64_t c_unit_stride, double* gen_sum,
+                      const int32_t* gen_count, const void* k_new,
+                      const void* v_new, void* k_cache, void* v_cache,
+                      int64_t cache_unit_stride, dhsa_layout layout, int U, int G,
+                      int D, int agg, double* scores, int64_t sc_stride,
+                      dhsa_stream_t stream);
+
+/* K4 — decode selection: the causal token-budget Top-K with forced self and
+ * lower-index tie-break (masks.topk_row, masks.py:103-122) applied to the
+ * block-constant upsampled row (masks.py:168-169), computed exactly as a walk
+ * over chunks ordered by (score desc, chunk asc) with a weighted radix select.
+ * Row i = plen[u] + gen_count[u] (the newest token).  Output: the selected
+ * token ranges split into tiles of at most `tile_tokens` tokens, sorted by
+ * start, followed by the self tile (i, 1).  tiles[s*tile_cap + t] = {start,
+ * count} for selection row s (s = u for aggregated scores, s = u*G+j for
+ * per-head scores; heads_per_unit = 1 or G), ntiles[s] = count of tiles. */
+int dhsa_decode_select(const double* scores, int64_t sc_stride, dhsa_layout layout,
+                       const int32_t* gen_count, int U, int heads_per_unit,
+                       int64_t budget, int tile_tokens, int32_t* tiles,
+                       int64_t tile_cap, int32_t* ntiles, dhsa_stream_t stream);
+
+/* K5/K6 — exact attention over selected token tiles: per q-head,
+ * softmax(K[idx] q / sqrt(D)) @ V[idx] (core.py:113-118) with an online
+ * softmax, split over `splits` CTAs per item and merged in-kernel (the last
+ * CTA of an item combines the (m, l, acc) partials).
+ * item s covers q rows s*GH .. s*GH+GH-1 and reads the cache of unit
+ * s / items_per_unit; tiles/ntiles as produced by dhsa_decode_select.
+ * dtype BF16: TMA-staged 128B-swizzled tiles + mma.sync (fp32 accumulate),
+ * D in {64, 128}, cache_unit_stride % 64 == 0.  dtype F32/F64: FFMA/DFMA with
+ * accumulation in the input precision, any D.
+ * out: [items*GH][D] in the input dtype (bf16 output for bf16).
+ * workspace: dhsa_attn_workspace_size bytes; counters: int32[items], zeroed
+ * once by the caller (the kernel re-arms them). */
+int64_t dhsa_attn_workspace_size(int dtype, int items, int GH, int D, int splits);
+int dhsa_attn(int dtype, const void* q, const void* k_cache, const void* v_cache,
+              int64_t cache_unit_stride, int64_t cache_rows, int items,
+              int items_per_unit, int GH, int D, const int32_t* tiles,
+              int64_t tile_cap, const int32_t* ntiles, int splits, void* out,
+              void* workspace, int32_t* counters, dhsa_stream_t stream);
+
+/* gen_count[u] += 1 for all units (masks.py:236). */
+int dhsa_decode_advance(int32_t* gen_count, int U, dhsa_stream_t stream);
+
+/* S_c = Q_c K_c^T for one head (chunk_repr.chunk_similarity,
+ * chunk_repr.py:97-103), fp64, no scaling.  qc: [n][D], kc: [m][D],
+ * out: [n][m]; batched over `heads` with the given strides (elements). */
+int dhsa_chunk_scores(const double* qc, const double* kc, int n, int m, int D,
+                      int heads, int64_t qc_head_stride, int64_t kc_head_stride,
+                      double* out, int64_t out_head_stride, dhsa_stream_t stream);
+
+/* Per-row selection of the prefill mask (masks.mask_from_chunk_scores,
+ * masks.py:125-140, i.e. topk_row on the upsampled row, :87-100): for each of
+ * `rows` query rows r with token index i = row_index[r] lying in chunk l,
+ * walk chunks 0..l with score row scores[l*sc_stride + c] (sc_stride = 0 uses
+ * one shared row, which is masks.topk_row on token scores when every chunk
+ * is one token), the diagonal chunk contributing [bounds[l], i).
+ * bounds: [n_chunks+1] int32.  Output as dhsa_decode_select. */
+int dhsa_rows_select(const double* scores, int64_t sc_stride, const int32_t* bounds,
+                     int n_chunks, const int32_t* row_index, int rows,
+                     int64_t budget, int tile_tokens, int32_t* tiles,
+                     int64_t tile_cap, int32_t* ntiles, dhsa_stream_t stream);
+
+/* f_upsample (masks.upsample, masks.py:87-100): out[i][j] = s[chunk(i)][chunk(j)]
+ * for an n x n chunk-score matrix and bounds [n+1]; out is L x L fp64.  Only
+ * the drop-in API uses it — the selection kernels never materialise it. */
+int dhsa_upsample(const double* scores, const int32_t* bounds, int n, int L,
+                  double* out, dhsa_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DHSA_B200_H */

@@ -1,0 +1,36 @@
+"""paper_2510_24606_b200 — B200-native (sm_100a) DHSA sparse-attention hot path.
+
+Drop-in for the hot-path surface of the reference package ``dhsa``
+(/root/reference/pkg/src/dhsa/__init__.py:7-49): the same names and
+signatures for chunk representations, sparsity masks (prefill and decode) and
+masked attention, computed by hand-written CUDA kernels in libdhsa_b200.so,
+plus the batched decode engine ``SparseDecoder`` that the benchmark drives.
+There is no CPU fallback: GPU entry points raise if the library or the
+device is missing.
+"""
+
+from .chunking import check_boundaries, extend_for_decode, static_boundaries
+from .core import TokenSequence, dense_attention
+from .chunk_repr import ChunkReps, aggregate_chunk, aggregate_rows, build_chunk_reps, \
+    chunk_similarity
+from .masks import CostCounters, DecodeSession, SparsityMask, decode_mask_row, \
+    mask_from_chunk_scores, prefill_mask, topk_row, upsample
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "TokenSequence", "dense_attention",
+    "check_boundaries", "static_boundaries", "extend_for_decode",
+    "ChunkReps", "aggregate_chunk", "aggregate_rows", "build_chunk_reps", "chunk_similarity",
+    "CostCounters", "SparsityMask", "upsample", "topk_row", "mask_from_chunk_scores",
+    "prefill_mask", "decode_mask_row", "DecodeSession",
+    "SparseDecoder",
+]
+
+
+def __getattr__(name):
+    if name == "SparseDecoder":
+        from .decode import SparseDecoder
+
+        return SparseDecoder
+    raise AttributeError(name)

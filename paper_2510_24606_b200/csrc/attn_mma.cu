@@ -1,0 +1,304 @@
+// K5 (bf16) — block-sparse decode attention: TMA-staged gathers of the
+// selected K/V tiles + mma.sync tensor-core tiles, online softmax, split-KV.
+//
+// Reference: dense_attention's per-row body (core.py:113-118) restricted to the
+// selected indices: softmax(K[idx] q / sqrt(d)) @ V[idx].
+//
+// One CTA = 4 consumer warps + 1 TMA producer warp and works on a contiguous
+// slice of one item's tile list (item = one kv group of GH q-heads, or one
+// q-head).  A tile is <= 64 consecutive cache tokens (one selected 64-block
+// or a piece of a selected range); the producer gathers its K and V rows with
+// 2-D TMA loads (64 rows x 128 B boxes, 128B swizzle, so ldmatrix is bank-
+// conflict free) into a STAGES-deep mbarrier ring.  Each consumer warp owns 16
+// tokens of the tile: S = Q K^T with Q (GH <= 8 heads, padded to 16 rows) as
+// the A operand kept in registers for the whole kernel, online softmax in the
+// log2 domain, then O += P V with P re-packed from the S accumulators as the
+// A operand (no shared-memory round trip).  Warps merge at the end, splits
+// merge in the last CTA (attn_common.cuh).  Tokens of a tile beyond its count
+// are masked; the KV cache is finite everywhere (zero-initialised), so the
+// masked rows contribute exactly 0.
+#include "attn_common.cuh"
+#include "capi.cuh"
+
+#include <cudaTypedefs.h>
+
+namespace dhsa {
+
+template <int D, int STAGES>
+__global__ __launch_bounds__(160) void attn_mma_kernel(
+    const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+    const __nv_bfloat16* __restrict__ q, int64_t cache_rows, int items_per_unit, int GH,
+    const int32_t* __restrict__ tiles, int64_t tile_cap, const int32_t* __restrict__ ntiles,
+    int splits, __nv_bfloat16* __restrict__ out, void* ws, int32_t* counters, float scale_log2) {
+  constexpr int NB = D / 64;                  // 128-byte column boxes per row
+  constexpr int BOX = 64 * 128;               // one box: 64 token rows x 128 B
+  constexpr int STAGE_BYTES = 2 * NB * BOX;   // K + V
+  constexpr int KS = D / 16;                  // k-steps of QK^T
+  constexpr int NT = D / 8;                   // n-tiles of PV
+
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full_bar[STAGES];
+  __shared__ __align__(8) uint64_t empty_bar[STAGES];
+
+  const int item = blockIdx.y, split = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int unit = item / items_per_unit;
+  const int nt_all = ntiles[item];
+  const int t_begin = (int)((int64_t)nt_all * split / splits);
+  const int n = (int)((int64_t)nt_all * (split + 1) / splits) - t_begin;
+  const int32_t* tl = tiles + ((int64_t)item * tile_cap + t_begin) * 2;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 4);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  float m = -INFINITY, l = 0.f;
+  float o[NT][4];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+
+  if (warp == 4) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      prefetch_tmap(&tmK);
+      prefetch_tmap(&tmV);
+      const int64_t row0 = (int64_t)unit * cache_rows;
+      for (int i = 0; i < n; ++i) {
+        const int s = i % STAGES;
+        if (i >= STAGES) mbar_wait(&empty_bar[s], ((i / STAGES) + 1) & 1);
+        const int row = (int)(row0 + __ldg(tl + 2 * i));
+        unsigned char* st = smem + s * STAGE_BYTES;
+        mbar_expect_tx(&full_bar[s], STAGE_BYTES);
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          tma_load_2d(st + b * BOX, &tmK, &full_bar[s], b * 64, row);
+          tma_load_2d(st + (NB + b) * BOX, &tmV, &full_bar[s], b * 64, row);
+        }
+      }
+    }
+  } else {
+    // ---------------- consumers ----------------
+    const int hrow = lane >> 2;  // head row of the A / C fragments
+    uint32_t qa[KS][2];
+    {
+      const bool live = hrow < GH;
+      const __nv_bfloat16* qrow = q + ((int64_t)item * GH + (live ? hrow : 0)) * D;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const int k0 = ks * 16 + 2 * (lane & 3);
+        qa[ks][0] = live ? *reinterpret_cast<const uint32_t*>(qrow + k0) : 0u;
+        qa[ks][1] = live ? *reinterpret_cast<const uint32_t*>(qrow + k0 + 8) : 0u;
+      }
+    }
+    // per-lane ldmatrix row/chunk selectors
+    const int mi = lane >> 3, r8 = lane & 7;
+    const int tok_k = warp * 16 + 8 * (mi >> 1) + r8;  // K: matrix (nt, khalf)
+    const int tok_v = warp * 16 + 8 * (mi & 1) + r8;   // V: matrix (tokhalf, ntile)
+
+    for (int i = 0; i < n; ++i) {
+      const int s = i % STAGES;
+      mbar_wait(&full_bar[s], (i / STAGES) & 1);
+      const int count = __ldg(tl + 2 * i + 1);
+      if (warp * 16 < count) {
+        const uint32_t kb = smem_u32(smem + s * STAGE_BYTES);
+        const uint32_t vb = kb + NB * BOX;
+        float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          const int dch = 2 * ks + (mi & 1);
+          const uint32_t addr =
+              kb + (dch >> 3) * BOX + tok_k * 128 + (((dch & 7) ^ (tok_k & 7)) << 4);
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4(addr, b0, b1, b2, b3);
+          mma_bf16(sc[0], qa[ks][0], 0u, qa[ks][1], 0u, b0, b1);
+          mma_bf16(sc[1], qa[ks][0], 0u, qa[ks][1], 0u, b2, b3);
+        }
+        // scores of head `hrow` for tokens warp*16 + 8*nt + 2*(lane&3) + {0,1}
+        float p[2][2];
+        float tmax = -INFINITY;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int tok = warp * 16 + 8 * nt + 2 * (lane & 3) + e;
+            const float v = tok < count ? sc[nt][e] * scale_log2 : -INFINITY;
+            p[nt][e] = v;
+            tmax = fmaxf(tmax, v);
+          }
+        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
+        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
+        const float mn = fmaxf(m, tmax);
+        const float corr = exp2f(m - mn);
+        float psum = 0.f;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            p[nt][e] = exp2f(p[nt][e] - mn);
+            psum += p[nt][e];
+          }
+        l = l * corr + psum;
+        m = mn;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          o[j][0] *= corr;
+          o[j][1] *= corr;
+        }
+        const uint32_t pa0 = pack_bf16(p[0][0], p[0][1]);
+        const uint32_t pa2 = pack_bf16(p[1][0], p[1][1]);
+#pragma unroll
+        for (int np = 0; np < NT / 2; ++np) {
+          const int dch = 2 * np + (mi >> 1);
+          const uint32_t addr =
+              vb + (dch >> 3) * BOX + tok_v * 128 + (((dch & 7) ^ (tok_v & 7)) << 4);
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4_t(addr, b0, b1, b2, b3);
+          mma_bf16(o[2 * np], pa0, 0u, pa2, 0u, b0, b1);
+          mma_bf16(o[2 * np + 1], pa0, 0u, pa2, 0u, b2, b3);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[s]);
+    }
+    l += __shfl_xor_sync(0xffffffffu, l, 1);
+    l += __shfl_xor_sync(0xffffffffu, l, 2);
+  }
+  __syncthreads();
+  // All TMA traffic has been consumed: the stage ring is reused for the merge.
+  const int rec = D + 2;
+  float* red = reinterpret_cast<float*>(smem);  // [4 warps][GH][D+2]
+  if (warp < 4) {
+    const int h = lane >> 2;
+    if (h < GH) {
+      float* r = red + (warp * GH + h) * rec;
+      if ((lane & 3) == 0) {
+        r[0] = m;
+        r[1] = l;
+      }
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        r[2 + j * 8 + 2 * (lane & 3)] = o[j][0];
+        r[2 + j * 8 + 2 * (lane & 3) + 1] = o[j][1];
+      }
+    }
+  }
+  __syncthreads();
+  const bool direct = (splits == 1);
+  for (int hd = threadIdx.x; hd < GH * D; hd += blockDim.x) {
+    const int h = hd / D, d = hd - h * D;
+    float mstar = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) mstar = fmaxf(mstar, red[(w * GH + h) * rec]);
+    float lsum = 0.f, a = 0.f;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const float* r = red + (w * GH + h) * rec;
+      if (r[0] == -INFINITY) continue;
+      const float wgt = exp2f(r[0] - mstar);
+      lsum += wgt * r[1];
+      a += wgt * r[2 + d];
+    }
+    if (direct) {
+      out[((int64_t)item * GH + h) * D + d] = __float2bfloat16_rn(a / lsum);
+    } else {
+      float* p = partial_ptr<float>(ws, item, split, splits, h, GH, D);
+      if (d == 0) {
+        p[0] = mstar;
+        p[1] = lsum;
+      }
+      p[2 + d] = a;
+    }
+  }
+  if (direct) return;
+  if (split_arrive(counters, item, splits))
+    merge_partials<__nv_bfloat16, float>(ws, item, splits, GH, D, out);
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2-D view [rows][D] of a bf16 cache; 64 x 64-element boxes, 128B swizzle.
+static int make_map(CUtensorMap* map, const void* base, int64_t rows, int D) {
+  auto enc = get_encode();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return DHSA_ECUDA;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)D * 2};
+  cuuint32_t box[2] = {64, 64};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return DHSA_ECUDA;
+  }
+  return DHSA_OK;
+}
+
+template <int D, int STAGES>
+static int launch(const CUtensorMap& mk, const CUtensorMap& mv, const void* q, int64_t cache_rows,
+                  int items, int ipu, int GH, const int32_t* tiles, int64_t cap,
+                  const int32_t* nt, int splits, void* out, void* ws, int32_t* cnt,
+                  cudaStream_t s) {
+  constexpr int STAGE_BYTES = 2 * (D / 64) * 64 * 128;
+  const size_t smem = (size_t)STAGES * STAGE_BYTES + 1024;
+  cudaError_t e = cudaFuncSetAttribute(attn_mma_kernel<D, STAGES>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) {
+    set_error("dhsa_attn(bf16): %s", cudaGetErrorString(e));
+    return DHSA_ECUDA;
+  }
+  const float scale_log2 = (float)(1.4426950408889634 / sqrt((double)D));
+  dim3 grid((unsigned)splits, (unsigned)items);
+  attn_mma_kernel<D, STAGES><<<grid, 160, smem, s>>>(
+      mk, mv, (const __nv_bfloat16*)q, cache_rows, ipu, GH, tiles, cap, nt, splits,
+      (__nv_bfloat16*)out, ws, cnt, scale_log2);
+  return check_launch("dhsa_attn(bf16)");
+}
+
+int attn_mma_bf16(const void* q, const void* k_cache, const void* v_cache,
+                  int64_t cache_unit_stride, int64_t cache_rows, int items, int items_per_unit,
+                  int GH, int D, const int32_t* tiles, int64_t tile_cap, const int32_t* ntiles,
+                  int splits, void* out, void* ws, int32_t* counters, cudaStream_t s) {
+  DHSA_REQUIRE(D == 64 || D == 128, "dhsa_attn(bf16): D must be 64 or 128, got %d", D);
+  DHSA_REQUIRE(cache_unit_stride == cache_rows * D,
+               "dhsa_attn(bf16): cache units must be dense [rows][D]");
+  DHSA_REQUIRE(((uintptr_t)k_cache & 15) == 0 && ((uintptr_t)v_cache & 15) == 0 &&
+                   ((uintptr_t)q & 3) == 0,
+               "dhsa_attn(bf16): misaligned pointers");
+  const int units = (items + items_per_unit - 1) / items_per_unit;
+  const int64_t rows = (int64_t)units * cache_rows;
+  DHSA_REQUIRE(rows < (1ll << 31), "dhsa_attn(bf16): cache too large for 32-bit TMA rows");
+  CUtensorMap mk, mv;
+  int rc = make_map(&mk, k_cache, rows, D);
+  if (rc) return rc;
+  rc = make_map(&mv, v_cache, rows, D);
+  if (rc) return rc;
+  if (D == 128)
+    return launch<128, 3>(mk, mv, q, cache_rows, items, items_per_unit, GH, tiles, tile_cap,
+                          ntiles, splits, out, ws, counters, s);
+  return launch<64, 6>(mk, mv, q, cache_rows, items, items_per_unit, GH, tiles, tile_cap, ntiles,
+                       splits, out, ws, counters, s);
+}
+
+}  // namespace dhsa

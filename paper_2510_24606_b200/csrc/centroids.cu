@@ -1,0 +1,77 @@
+// K1 — chunk centroids, fp64, bit-exact with the reference.
+//
+// Reference: chunk_repr.aggregate_rows (chunk_repr.py:57-68) calls
+// aggregate_chunk (:38-54) = sequential_sum(t) / sqrt(n); sequential_sum
+// (:29-35) starts from 0.0 and adds one row at a time in token order.  Every
+// thread here owns one (chunk, dimension) pair and performs exactly that
+// sequence of IEEE fp64 additions followed by one correctly rounded division
+// by sqrt((double)n), so the result is bit-identical for any input dtype
+// (bf16/fp32 upcasts are exact).  Loads are coalesced across the dimension
+// axis (consecutive threads = consecutive dims of the same token row).
+#include "capi.cuh"
+
+namespace dhsa {
+
+template <typename T>
+__global__ __launch_bounds__(256) void centroids_kernel(const T* __restrict__ x,
+                                                        int64_t x_unit_stride, int D,
+                                                        Layout lay, int normalize,
+                                                        double* __restrict__ out,
+                                                        int64_t out_unit_stride) {
+  const int u = blockIdx.y;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = (int)(idx / D);
+  const int d = (int)(idx - (int64_t)c * D);
+  if (c >= lay.num_chunks(u)) return;
+  int lo, hi;
+  lay.chunk(u, c, lo, hi);
+  const T* src = x + (int64_t)u * x_unit_stride + (int64_t)lo * D + d;
+  double acc = 0.0;
+  int t = 0;
+  const int n = hi - lo;
+  // 8 independent loads in flight, then the additions in token order.
+  for (; t + 8 <= n; t += 8) {
+    double v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = to_f64(src[(int64_t)(t + k) * D]);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc = __dadd_rn(acc, v[k]);
+  }
+  for (; t < n; ++t) acc = __dadd_rn(acc, to_f64(src[(int64_t)t * D]));
+  out[(int64_t)u * out_unit_stride + (int64_t)c * D + d] =
+      normalize ? __ddiv_rn(acc, __dsqrt_rn((double)n)) : acc;
+}
+
+}  // namespace dhsa
+
+using namespace dhsa;
+
+extern "C" int dhsa_centroids(int dtype, const void* x, int64_t x_unit_stride, int D, int U,
+                              dhsa_layout layout, int normalize, double* out,
+                              int64_t out_unit_stride, dhsa_stream_t stream) {
+  DHSA_REQUIRE(x && out && D >= 1 && U >= 1, "dhsa_centroids: bad arguments");
+  DHSA_REQUIRE(valid_layout(layout) && layout.max_chunks >= 1, "dhsa_centroids: bad layout");
+  const int64_t work = (int64_t)layout.max_chunks * D;
+  dim3 grid((unsigned)((work + 255) / 256), (unsigned)U);
+  cudaStream_t s = (cudaStream_t)stream;
+  Layout lay(layout);
+  switch (dtype) {
+    case DHSA_F64:
+      centroids_kernel<double><<<grid, 256, 0, s>>>((const double*)x, x_unit_stride, D, lay, normalize, out,
+                                                    out_unit_stride);
+      break;
+    case DHSA_F32:
+      centroids_kernel<float><<<grid, 256, 0, s>>>((const float*)x, x_unit_stride, D, lay, normalize, out,
+                                                   out_unit_stride);
+      break;
+    case DHSA_BF16:
+      centroids_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)x,
+                                                           x_unit_stride, D, lay, normalize, out,
+                                                           out_unit_stride);
+      break;
+    default:
+      set_error("dhsa_centroids: unknown dtype %d", dtype);
+      return DHSA_EINVAL;
+  }
+  return check_launch("dhsa_centroids");
+}

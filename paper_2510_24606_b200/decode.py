@@ -1,0 +1,173 @@
+"""Batched DHSA decode engine — the north-star hot path.
+
+One decode step for a batch of B sequences with Hq query heads sharing Hkv
+key/value heads (group size G = Hq / Hkv), each sequence holding a prompt of
+P_b tokens split into static ``block``-token chunks plus g generated tokens:
+
+  1. ``dhsa_decode_score``  fp64 q . centroid scores for every prompt chunk
+     and the generated chunk (Algorithm 2, masks.py:153-173), reduced over
+     the G heads of a group (harness.py:288-306 max/mean) or kept per head;
+     folds the new key into the fp64 running sum and appends k/v to the cache.
+  2. ``dhsa_decode_select`` the exact token-budget Top-K (masks.py:103-122)
+     as a weighted radix-select chunk walk -> tiles of <= 64 tokens + self.
+  3. ``dhsa_attn``          softmax attention of the G heads over the selected
+     tiles (core.py:113-118): TMA + mma.sync for bf16, FFMA for fp32,
+     split-KV with an in-kernel (m, l, acc) merge.
+  4. ``dhsa_decode_advance`` g += 1.
+
+Memory layout in HBM (all dense, allocated once):
+  K/V cache  [B, Hkv, L_cap, D]  (dtype; = block-contiguous [B,Hkv,L/64,64,D])
+  centroids  [B, Hkv, N_c, D]     fp64 (built once per prompt by K1)
+  gen_sum    [B, Hkv, D]          fp64, gen_count/plen [B*Hkv] int32
+  scores     [B*Hsel, N_c+1]      fp64, tiles [B*Hsel, cap, 2] int32
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import _lib
+
+_DT = {torch.bfloat16: _lib.BF16, torch.float32: _lib.F32, torch.float64: _lib.F64}
+
+
+def default_splits(items: int, tiles_per_item: int, sms: int = 148) -> int:
+    """Split-KV factor: ~8 tiles per CTA, enough CTAs to fill the SMs twice."""
+    by_work = max(1, math.ceil(tiles_per_item / 8))
+    by_fill = max(1, math.ceil(2 * sms / max(items, 1)))
+    return int(max(1, min(16, max(min(by_work, 8), min(by_fill, by_work)))))
+
+
+class SparseDecoder:
+    """Batched sparse decode over a KV cache resident in HBM.
+
+    ``budget`` is the reference's token budget (masks.topk_row); with
+    ``top_k`` blocks it defaults to ``top_k * block + 1`` (K whole blocks plus
+    self).  ``agg`` selects group-shared selection ("max" / "mean", one
+    selection per kv head, harness.aggregated_chunk_scores semantics) or
+    per-q-head selection ("none", one DecodeSession per head)."""
+
+    def __init__(self, batch, q_heads, kv_heads, head_dim, max_len, *, block=64, top_k=64,
+                 budget=None, dtype=torch.bfloat16, agg="max", tile=64, splits=None,
+                 device=None):
+        _lib.require_cuda()
+        if q_heads % kv_heads:
+            raise ValueError("q_heads must be a multiple of kv_heads")
+        if dtype not in _DT:
+            raise ValueError(f"unsupported dtype {dtype}")
+        if agg not in _lib.AGG:
+            raise ValueError(f"unknown aggregation {agg!r}")
+        self.B, self.Hq, self.Hkv, self.D = batch, q_heads, kv_heads, head_dim
+        self.G = q_heads // kv_heads
+        self.U = batch * kv_heads
+        self.block = int(block)
+        self.budget = int(budget if budget is not None else top_k * block + 1)
+        if self.budget < 1:
+            raise ValueError("budget must be >= 1")
+        self.dtype = dtype
+        self.code = _DT[dtype]
+        self.agg = agg
+        self.per_head = agg == "none"
+        self.tile = int(tile)
+        self.dev = torch.device(device) if device is not None else torch.device("cuda")
+        self.L_cap = ((int(max_len) + 64 - 1) // 64) * 64 + 64
+        self.nc_cap = (int(max_len) + self.block - 1) // self.block
+        kw = dict(device=self.dev)
+        self.k_cache = torch.zeros(batch, kv_heads, self.L_cap, head_dim, dtype=dtype, **kw)
+        self.v_cache = torch.zeros_like(self.k_cache)
+        self.centroids = torch.zeros(batch, kv_heads, self.nc_cap, head_dim, dtype=torch.float64, **kw)
+        self.gen_sum = torch.zeros(self.U, head_dim, dtype=torch.float64, **kw)
+        self.gen_count = torch.zeros(self.U, dtype=torch.int32, **kw)
+        self.plen = torch.zeros(self.U, dtype=torch.int32, **kw)
+        self.items = self.U * self.G if self.per_head else self.U
+        self.GH = 1 if self.per_head else self.G
+        self.scores = torch.empty(self.items, self.nc_cap + 1, dtype=torch.float64, **kw)
+        r = self.budget - 1
+        self.tile_cap = min(self.nc_cap + 1, r) + r // self.tile + 2
+        self.tiles = torch.zeros(self.items, self.tile_cap, 2, dtype=torch.int32, **kw)
+        self.ntiles = torch.zeros(self.items, dtype=torch.int32, **kw)
+        tiles_per_item = math.ceil(r / self.tile) + 2
+        self.splits = int(splits) if splits else default_splits(self.items, tiles_per_item)
+        nbytes = _lib.load().dhsa_attn_workspace_size(self.code, self.items, self.GH, head_dim,
+                                                      self.splits)
+        self.ws = torch.empty(max(nbytes, 8), dtype=torch.uint8, **kw)
+        self.counters = torch.zeros(self.items, dtype=torch.int32, **kw)
+        self.max_prompt = 0
+        self.steps = 0
+
+    # ------------------------------------------------------------------
+    def _layout(self):
+        return _lib.layout(plen=self.plen, block=self.block, max_chunks=self.max_chunks)
+
+    def prefill(self, keys, values, prompt_len=None):
+        """Load prompt K/V [B, Hkv, P, D] into the cache and build the fp64
+        centroid cache (K1, chunk_repr.aggregate_rows semantics)."""
+        P = keys.shape[2] if prompt_len is None else int(prompt_len)
+        if P < 1 or P + 1 > self.L_cap - 64:
+            raise ValueError("prompt does not fit the cache")
+        self.k_cache[:, :, :P].copy_(keys[:, :, :P])
+        self.v_cache[:, :, :P].copy_(values[:, :, :P])
+        self.plen.fill_(P)
+        self.gen_count.zero_()
+        self.gen_sum.zero_()
+        self.max_prompt = P
+        self.max_chunks = (P + self.block - 1) // self.block
+        self.steps = 0
+        st = _lib.stream_handle()
+        _lib.call("dhsa_centroids", self.code, _lib.ptr(self.k_cache), self.L_cap * self.D,
+                  self.D, self.U, self._layout(), 1, _lib.ptr(self.centroids),
+                  self.nc_cap * self.D, st)
+
+    def step(self, q, k_new, v_new, out=None):
+        """One decode step.  q [B, Hq, D], k_new/v_new [B, Hkv, D] (cache
+        dtype, contiguous, on device).  Returns attention output [B, Hq, D]."""
+        if self.max_prompt + self.steps + 1 > self.L_cap - 64:
+            raise RuntimeError("KV cache capacity exhausted")
+        if out is None:
+            out = torch.empty(self.B, self.Hq, self.D, dtype=self.dtype, device=self.dev)
+        self.launch(q, k_new, v_new, out)
+        self.steps += 1
+        return out
+
+    def launch(self, q, k_new, v_new, out, stream=None):
+        """Enqueue the four kernels of one step (graph-capturable)."""
+        st = _lib.stream_handle(stream)
+        lay = self._layout()
+        agg = _lib.AGG[self.agg]
+        _lib.call("dhsa_decode_score", self.code, _lib.ptr(q), _lib.ptr(self.centroids),
+                  self.nc_cap * self.D, _lib.ptr(self.gen_sum), _lib.ptr(self.gen_count),
+                  _lib.ptr(k_new), _lib.ptr(v_new), _lib.ptr(self.k_cache),
+                  _lib.ptr(self.v_cache), self.L_cap * self.D, lay, self.U, self.G, self.D, agg,
+                  _lib.ptr(self.scores), self.nc_cap + 1, st)
+        _lib.call("dhsa_decode_select", _lib.ptr(self.scores), self.nc_cap + 1, lay,
+                  _lib.ptr(self.gen_count), self.U, self.G if self.per_head else 1, self.budget,
+                  self.tile, _lib.ptr(self.tiles), self.tile_cap, _lib.ptr(self.ntiles), st)
+        _lib.call("dhsa_attn", self.code, _lib.ptr(q), _lib.ptr(self.k_cache),
+                  _lib.ptr(self.v_cache), self.L_cap * self.D, self.L_cap, self.items,
+                  self.G if self.per_head else 1, self.GH, self.D, _lib.ptr(self.tiles),
+                  self.tile_cap, _lib.ptr(self.ntiles), self.splits, _lib.ptr(out),
+                  _lib.ptr(self.ws), _lib.ptr(self.counters), st)
+        _lib.call("dhsa_decode_advance", _lib.ptr(self.gen_count), self.U, st)
+
+    # ------------------------------------------------------------------
+    def selection(self):
+        """Host copy of the last step's selection: list over selection rows of
+        (start, count) tiles (self tile last)."""
+        t = self.tiles.cpu().numpy()
+        n = self.ntiles.cpu().numpy()
+        return [t[i, : n[i]].copy() for i in range(self.items)]
+
+    def bytes_per_step(self) -> dict:
+        """Algorithmic (unique) HBM bytes of one step, the roofline numerator
+        (fp64 centroids + selected K/V rows + q/o)."""
+        esz = torch.finfo(self.dtype).bits // 8
+        P, g = self.max_prompt, self.steps
+        nc = (P + self.block - 1) // self.block
+        cent = self.U * nc * self.D * 8
+        sel_tokens = min(self.budget, P + g + 1)
+        per_sel = sel_tokens * self.D * esz * 2
+        kv = (self.items if self.per_head else self.U) * per_sel
+        qo = 2 * self.B * self.Hq * self.D * esz
+        return {"centroids": cent, "kv": kv, "qo": qo, "total": cent + kv + qo}

@@ -1,0 +1,139 @@
+"""GPU parity of the batched decode engine (SparseDecoder) — the north-star
+path — against the CPU oracle and the reference's golden C1 vectors.
+
+Selections: bit-exact indices.  Outputs: max|o - o_ref| <= tol * max|o_ref|
+per (sequence, q-head), tol = 2e-2 (bf16), 1e-5 (fp32), 1e-12 (fp64), against
+the float64 reference row body (core.py:113-118)."""
+
+import numpy as np
+import pytest
+import torch
+
+import golden_io as G
+from decode_harness import TOL, make_inputs, run_and_check, tiles_to_idx
+from oracle import dhsa_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _dec(**kw):
+    from paper_2510_24606_b200.decode import SparseDecoder
+    return SparseDecoder(**kw)
+
+
+def test_c1_golden_fp32():
+    """C1 demo shape (8 heads, d=64, L=4096, block 64, top-k 16) vs the
+    reference's own DecodeSession rows and attention outputs."""
+    gd = G.c1_golden()
+    H, L, d, steps = gd["H"], gd["L"], gd["d"], gd["steps"]
+    dec = _dec(batch=1, q_heads=H, kv_heads=H, head_dim=d, max_len=L + steps, block=64, top_k=16,
+               dtype=torch.float32, agg="max")
+    k = torch.from_numpy(gd["k"]).unsqueeze(0).cuda()
+    v = torch.from_numpy(gd["v"]).unsqueeze(0).cuda()
+    q = torch.from_numpy(gd["q"]).unsqueeze(0).cuda()
+    dec.prefill(k[:, :, :L], v[:, :, :L])
+    for s in range(steps):
+        t = L + s
+        out = dec.step(q[:, :, t].contiguous(), k[:, :, t].contiguous(), v[:, :, t].contiguous())
+        sel = dec.selection()
+        o = out.double().cpu().numpy()[0]
+        for h in range(H):
+            assert np.array_equal(tiles_to_idx(sel[h]), G.ranges_to_idx(gd["rows"][(h, s)], t))
+            ref = gd["out"][h, s]
+            assert np.abs(o[h] - ref).max() <= 1e-5 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32, torch.float64])
+@pytest.mark.parametrize("agg", ["max", "mean", "none"])
+def test_gqa_decode_small(dtype, agg):
+    B, Hq, Hkv, D, P, steps = 2, 8, 2, 128, 1000, 5
+    t, host = make_inputs(B, Hq, Hkv, D, P, steps, dtype, seed=1)
+    dec = _dec(batch=B, q_heads=Hq, kv_heads=Hkv, head_dim=D, max_len=P + steps, block=64,
+               top_k=4, dtype=dtype, agg=agg)
+    worst = run_and_check(dec, t, host, P, steps, agg)
+    assert worst <= TOL[dtype], worst
+
+
+@pytest.mark.parametrize("budget", [1, 2, 63, 64, 65, 200, 257, 5000])
+def test_budget_edge_cases_bf16(budget):
+    """Budgets that cut chunks (K*64 and odd values), budget 1 (self only)
+    and a budget above the context (everything kept)."""
+    B, Hq, Hkv, D, P, steps = 1, 4, 1, 64, 700, 3
+    t, host = make_inputs(B, Hq, Hkv, D, P, steps, torch.bfloat16, seed=2)
+    dec = _dec(batch=B, q_heads=Hq, kv_heads=Hkv, head_dim=D, max_len=P + steps, block=64,
+               budget=budget, dtype=torch.bfloat16, agg="max")
+    worst = run_and_check(dec, t, host, P, steps, "max")
+    assert worst <= 2e-2
+
+
+@pytest.mark.parametrize("kind", ["int", "ties"])
+def test_exact_ties(kind):
+    """Integer-valued inputs: every fp64 score is exact, so ties between
+    chunks are real and must resolve to the lower index."""
+    B, Hq, Hkv, D, P, steps = 2, 4, 2, 64, 640, 4
+    t, host = make_inputs(B, Hq, Hkv, D, P, steps, torch.bfloat16, seed=3, kind=kind)
+    dec = _dec(batch=B, q_heads=Hq, kv_heads=Hkv, head_dim=D, max_len=P + steps, block=64,
+               top_k=3, dtype=torch.bfloat16, agg="max")
+    run_and_check(dec, t, host, P, steps, "max", check_out=False)
+
+
+def test_long_generated_chunk():
+    """The generated chunk grows past a block and competes in the walk."""
+    B, Hq, Hkv, D, P, steps = 1, 4, 1, 128, 256, 150
+    t, host = make_inputs(B, Hq, Hkv, D, P, steps, torch.bfloat16, seed=4)
+    # make generated keys resemble the queries so the gen chunk is selected
+    t["k"][:, :, P:] = t["q"][:, :1] * 2
+    host["k"] = t["k"].to(torch.float64).numpy()
+    dec = _dec(batch=B, q_heads=Hq, kv_heads=Hkv, head_dim=D, max_len=P + steps, block=64,
+               budget=130, dtype=torch.bfloat16, agg="max")
+    worst = run_and_check(dec, t, host, P, steps, "max")
+    assert worst <= 2e-2
+
+
+def test_ragged_prompt_and_dims():
+    """Prompt not a multiple of the block; D=64 and group size 8."""
+    B, Hq, Hkv, D, P, steps = 3, 8, 1, 64, 1234, 3
+    t, host = make_inputs(B, Hq, Hkv, D, P, steps, torch.bfloat16, seed=5)
+    dec = _dec(batch=B, q_heads=Hq, kv_heads=Hkv, head_dim=D, max_len=P + steps, block=64,
+               top_k=5, dtype=torch.bfloat16, agg="max")
+    assert run_and_check(dec, t, host, P, steps, "max") <= 2e-2
+
+
+def test_c2_shape_sampled_units():
+    """C2 shape (B=8, 32q/8kv, d=128, L=32K, block 64, top-k 64): every unit's
+    selection exact, outputs checked on sampled units."""
+    B, Hq, Hkv, D, P, steps = 8, 32, 8, 128, 32768, 2
+    t, host = make_inputs(B, Hq, Hkv, D, P, steps, torch.bfloat16, seed=6)
+    dec = _dec(batch=B, q_heads=Hq, kv_heads=Hkv, head_dim=D, max_len=P + steps, block=64,
+               top_k=64, dtype=torch.bfloat16, agg="max")
+    worst = run_and_check(dec, t, host, P, steps, "max", check_units=[0, 9, 35, 63])
+    assert worst <= 2e-2
+
+
+def test_step_graph_replay_matches_eager():
+    """The four kernels of a step are CUDA-graph capturable; a replayed
+    step gives the same selection and output as an eager one."""
+    from paper_2510_24606_b200.decode import SparseDecoder
+    B, Hq, Hkv, D, P = 2, 8, 2, 128, 2048
+    t, _ = make_inputs(B, Hq, Hkv, D, P, 4, torch.bfloat16, seed=7)
+    outs = []
+    for mode in ("eager", "graph"):
+        dec = SparseDecoder(B, Hq, Hkv, D, P + 4, top_k=8, dtype=torch.bfloat16)
+        dec.prefill(t["k"][:, :, :P].cuda(), t["v"][:, :, :P].cuda())
+        q = t["q"][:, :, 0].contiguous().cuda()
+        kn = t["k"][:, :, P].contiguous().cuda()
+        vn = t["v"][:, :, P].contiguous().cuda()
+        out = torch.empty(B, Hq, D, dtype=torch.bfloat16, device="cuda")
+        if mode == "eager":
+            dec.launch(q, kn, vn, out)
+        else:
+            s = torch.cuda.Stream()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                dec.launch(q, kn, vn, out, stream=s)
+            g.replay()
+        torch.cuda.synchronize()
+        outs.append((out.clone(), [x.copy() for x in dec.selection()]))
+    assert torch.equal(outs[0][0], outs[1][0])
+    for a, b in zip(outs[0][1], outs[1][1]):
+        assert np.array_equal(a, b)

@@ -1,0 +1,172 @@
+"""Host-side logic that runs without a GPU: boundary lists, argument
+validation (same ValueError behaviour as the reference, raised before any
+device work), the C-ABI library exports, and the split heuristics."""
+
+import ctypes
+import os
+
+import numpy as np
+import pytest
+
+import paper_2510_24606_b200 as P
+from paper_2510_24606_b200 import _lib
+from paper_2510_24606_b200.core import rows_to_tiles
+
+
+# ---- chunking.py (reference tests/test_chunking.py semantics) -------------
+
+def test_static_boundaries():
+    assert P.static_boundaries(10, 4) == [0, 4, 8, 10]
+    assert P.static_boundaries(8, 4) == [0, 4, 8]
+    assert P.static_boundaries(3, 8) == [0, 3]
+    with pytest.raises(ValueError):
+        P.static_boundaries(0, 4)
+    with pytest.raises(ValueError):
+        P.static_boundaries(4, 0)
+
+
+def test_check_boundaries():
+    assert P.check_boundaries([0, 2, 5], 5) == [0, 2, 5]
+    for bad in ([0], [1, 3], [0, 3, 3], [0, 4, 2]):
+        with pytest.raises(ValueError):
+            P.check_boundaries(bad)
+    with pytest.raises(ValueError):
+        P.check_boundaries([0, 3], 4)
+
+
+def test_extend_for_decode():
+    assert P.extend_for_decode([0, 8], 9) == [0, 8, 9]
+    assert P.extend_for_decode([0, 4, 8], 11) == [0, 4, 8, 10, 11]
+    assert P.extend_for_decode([0, 8], 10) == [0, 8, 9, 10]
+    with pytest.raises(ValueError):
+        P.extend_for_decode([0, 8], 8)
+    for total in (9, 10, 17, 40):
+        b = P.extend_for_decode([0, 3, 8], total)
+        assert P.check_boundaries(b, total) == b
+
+
+# ---- validation before any device work ------------------------------------
+
+def test_topk_row_rejects_bad_arguments(rng):
+    with pytest.raises(ValueError):
+        P.topk_row(rng.standard_normal(4), 2, 0)
+    with pytest.raises(ValueError):
+        P.topk_row(rng.standard_normal(3), 5, 2)
+
+
+def test_sparsity_mask_validation():
+    m = P.SparsityMask(length=3, rows=([0], [0, 1], [2]))
+    assert m.row_sizes().tolist() == [1, 2, 1]
+    want = np.array([[1, 0, 0], [1, 1, 0], [0, 0, 1]], dtype=bool)
+    assert np.array_equal(m.to_dense(), want)
+    for rows in (([0, 1], [1]), ([0], [0]), ([0], [1, 0]), ([0], [0, 0, 1])):
+        with pytest.raises(ValueError):
+            P.SparsityMask(length=2, rows=rows)
+    with pytest.raises(ValueError):
+        P.SparsityMask(length=3, rows=([0], [0, 1]))
+
+
+def test_token_sequence_validation(rng):
+    q = rng.standard_normal((3, 2))
+    q[1, 0] = np.nan
+    with pytest.raises(ValueError):
+        P.TokenSequence(q, np.zeros((3, 2)), np.zeros((3, 2)))
+    with pytest.raises(ValueError):
+        P.TokenSequence(rng.standard_normal((3, 2)), rng.standard_normal((4, 2)),
+                        rng.standard_normal((3, 2)))
+    with pytest.raises(ValueError):
+        P.TokenSequence(rng.standard_normal(3), rng.standard_normal(3), rng.standard_normal(3))
+    s = P.TokenSequence(*(rng.standard_normal((7, 5)) for _ in range(3)))
+    assert (s.length, s.dim) == (7, 5)
+
+
+def test_dense_attention_mask_validation(rng):
+    seq = P.TokenSequence(*(rng.standard_normal((4, 2)) for _ in range(3)))
+    for rows in ([[0], [1], [2, 3], [3]], [[0], [0], [0, 2], [3]], [[0], []],
+                 [[0], [0, 1]]):
+        with pytest.raises(ValueError):
+            P.dense_attention(seq, rows)
+
+
+def test_upsample_and_mask_shape_validation(rng):
+    with pytest.raises(ValueError):
+        P.upsample(rng.standard_normal((2, 2)), [0, 3, 6, 9])
+    with pytest.raises(ValueError):
+        P.mask_from_chunk_scores(rng.standard_normal((2, 2)), [0, 3, 6, 9], 3)
+
+
+def test_aggregate_chunk_validation(rng):
+    with pytest.raises(ValueError):
+        P.aggregate_chunk(np.zeros((0, 3)))
+    t = rng.standard_normal((4, 3))
+    with pytest.raises(ValueError):
+        P.aggregate_chunk(t, valid_count=5)
+    with pytest.raises(ValueError):
+        P.aggregate_chunk(t, valid_count=0)
+
+
+def test_decode_mask_row_validation(rng):
+    with pytest.raises(ValueError):
+        P.decode_mask_row([0, 4], np.zeros((1, 3)), np.zeros((0, 3)), np.zeros(3), 5, 2)
+    with pytest.raises(ValueError):
+        P.decode_mask_row([0, 4], np.zeros((1, 3)), np.zeros((2, 3)), np.zeros(3), 5, 2)
+
+
+def test_rows_to_tiles():
+    tiles, n = rows_to_tiles([np.array([0]), np.array([0, 1, 2, 5, 6, 9])], tile=2)
+    assert n.tolist() == [1, 4]
+    assert tiles[1, :4].tolist() == [[0, 2], [2, 1], [5, 2], [9, 1]]
+
+
+# ---- the C ABI --------------------------------------------------------------
+
+def test_library_exports_every_header_symbol():
+    lib = _lib.load()
+    syms = _lib.header_symbols()
+    assert len(syms) >= 10
+    for name in syms:
+        assert hasattr(lib, name), name
+    assert lib.dhsa_version() == 1
+    # ctypes signature table covers the header exactly
+    assert set(_lib._SIGS) == set(syms)
+
+
+def test_library_is_sm100a():
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _lib.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_workspace_size_formula():
+    lib = _lib.load()
+    assert lib.dhsa_attn_workspace_size(_lib.BF16, 256, 4, 128, 1) == 0
+    assert lib.dhsa_attn_workspace_size(_lib.BF16, 256, 4, 128, 8) == 4 * 256 * 8 * 4 * 130
+    assert lib.dhsa_attn_workspace_size(_lib.F64, 3, 1, 5, 2) == 8 * 3 * 2 * 1 * 7
+
+
+def test_error_channel_without_device():
+    lib = _lib.load()
+    rc = lib.dhsa_decode_select(None, 0, _lib.Layout(), None, 1, 1, 5, 64, None, 1, None, None)
+    assert rc == -1
+    assert b"null pointer" in lib.dhsa_last_error()
+    rc = lib.dhsa_decode_select(ctypes.c_void_p(8), 0, _lib.Layout(), ctypes.c_void_p(8), 1, 1, 0,
+                                64, ctypes.c_void_p(8), 1, ctypes.c_void_p(8), None)
+    assert rc == -1
+    assert b"budget must be >= 1" in lib.dhsa_last_error()
+
+
+def test_default_splits():
+    from paper_2510_24606_b200.decode import default_splits
+    assert default_splits(256, 66) == 8
+    assert 1 <= default_splits(8, 18) <= 16
+    assert default_splits(10000, 3) == 1
+
+
+def test_no_oracle_import_in_product():
+    pkg = os.path.dirname(P.__file__)
+    for root, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith(".py"):
+                src = open(os.path.join(root, f)).read()
+                assert "oracle" not in src.replace("oracle/", ""), f
