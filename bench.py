@@ -217,7 +217,6 @@ def load_traffic():
 def run_gpu(args):
     import torch
 
-    from paper_2510_24606_b200 import _lib
     from paper_2510_24606_b200.decode import SparseDecoder
 
     world, rank, local = dist_setup()
@@ -228,7 +227,7 @@ def run_gpu(args):
     roll = args.roll_steps  # untimed replays before/after the timed steps (clock sampling)
     total_steps = W + S + 2 * roll + args.breakdown_steps + args.e2e_steps + 4
     dec = SparseDecoder(B, Hq, Hkv, D, L + total_steps, block=blk, top_k=K, dtype=dtype,
-                        agg="max")
+                        agg="max", scoring=args.scoring, splits=args.splits)
     gen = torch.Generator(device="cuda")
     gen.manual_seed(1234 + rank)
     # prompt K/V written straight into the cache, then the fp64 centroid build
@@ -282,47 +281,33 @@ def run_gpu(args):
     value = B * world * S / (ms / 1e3)
 
     # per-kernel breakdown (eager launches bracketed by events, same stream)
-    lib = _lib.load()
-    names = ["decode_score", "decode_select", "attn", "advance"]
-    acc = {n: 0.0 for n in names}
+    names = None
+    acc = {}
     nb = args.breakdown_steps
     for i in range(nb):
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        j = i % nslot
+        stg = dec.stages(qs[j], ks[j], vs[j], out, stream=stream)
+        names = [n for n, _ in stg]
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(stg) + 1)]
         with torch.cuda.stream(stream):
-            st = _lib.stream_handle(stream)
-            lay = dec._layout()
-            j = i % nslot
             ev[0].record(stream)
-            _lib.call("dhsa_decode_score", dec.code, _lib.ptr(qs[j]), _lib.ptr(dec.centroids),
-                      dec.nc_cap * D, _lib.ptr(dec.gen_sum), _lib.ptr(dec.gen_count),
-                      _lib.ptr(ks[j]), _lib.ptr(vs[j]), _lib.ptr(dec.k_cache),
-                      _lib.ptr(dec.v_cache), dec.L_cap * D, lay, dec.U, dec.G, D,
-                      _lib.AGG[dec.agg], _lib.ptr(dec.scores), dec.nc_cap + 1, st)
-            ev[1].record(stream)
-            _lib.call("dhsa_decode_select", _lib.ptr(dec.scores), dec.nc_cap + 1, lay,
-                      _lib.ptr(dec.gen_count), dec.U, 1, dec.budget, dec.tile,
-                      _lib.ptr(dec.tiles), dec.tile_cap, _lib.ptr(dec.ntiles), st)
-            ev[2].record(stream)
-            _lib.call("dhsa_attn", dec.code, _lib.ptr(qs[j]), _lib.ptr(dec.k_cache),
-                      _lib.ptr(dec.v_cache), dec.L_cap * D, dec.L_cap, dec.items, 1, dec.GH, D,
-                      _lib.ptr(dec.tiles), dec.tile_cap, _lib.ptr(dec.ntiles), dec.splits,
-                      _lib.ptr(out), _lib.ptr(dec.ws), _lib.ptr(dec.counters), st)
-            ev[3].record(stream)
-            _lib.call("dhsa_decode_advance", _lib.ptr(dec.gen_count), dec.U, st)
-            ev[4].record(stream)
+            for k_, (_, fn) in enumerate(stg):
+                fn()
+                ev[k_ + 1].record(stream)
         torch.cuda.synchronize()
         dec.steps += 1
         if i == 0:
             continue  # first eager launch pays one-time attribute setup
         for k_, n in enumerate(names):
-            acc[n] += ev[k_].elapsed_time(ev[k_ + 1])
+            acc[n] = acc.get(n, 0.0) + ev[k_].elapsed_time(ev[k_ + 1])
     cnt = max(1, nb - 1)
     us = {n: acc[n] / cnt * 1e3 for n in names}
     bytes_ = dec.bytes_per_step()
-    score_bytes = bytes_["centroids"] + B * Hq * D * 2 + dec.items * (dec.max_chunks + 1) * 8
+    score_name = names[0]
+    score_bytes = bytes_["centroids"] + B * Hq * D * 2
     attn_bytes = bytes_["kv"] + 2 * B * Hq * D * 2
-    kern_bytes = {"decode_score": score_bytes, "attn": attn_bytes}
-    dominant = max(("decode_score", "attn"), key=lambda n: us[n])
+    kern_bytes = {score_name: score_bytes, "attn": attn_bytes}
+    dominant = max((score_name, "attn"), key=lambda n: us[n])
     peak, peak_src = peaks()
     achieved = kern_bytes[dominant] / (us[dominant] * 1e-6) / 1e9
     traffic = load_traffic().get(name, {}).get(dominant)
@@ -362,7 +347,8 @@ def run_gpu(args):
                    "context": L, "block": blk, "top_k": K, "budget": K * blk + 1,
                    "selection": "group-shared max over q-heads", "parallelism": f"dp{world}",
                    "l2": "inputs larger than L2 (centroids 537 MB + selected KV 537 MB per step)",
-                   "graphs": "one CUDA graph per step (4 kernels)"},
+                   "graphs": f"one CUDA graph per step ({dec.kernels_per_step} kernels)",
+                   "scoring": dec.scoring},
         "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "algorithmic_bytes": kern_bytes[dominant]},
@@ -373,7 +359,7 @@ def run_gpu(args):
         "e2e": {"value": B * world / (e2e_ms / 1e3), "unit": "tokens/s",
                 "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "path": "SparseDecoder.step (ctypes C-ABI) with pinned host q/k/v -> o"},
-        "gpu_launches": 4 * S,
+        "gpu_launches": dec.kernels_per_step * S,
         "clocks": clk.summary(),
         "splits": dec.splits,
     }
@@ -425,6 +411,8 @@ def main():
     ap.add_argument("--breakdown-steps", type=int, default=6)
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--roll-steps", type=int, default=1500)
+    ap.add_argument("--scoring", default=None, choices=[None, "sketch", "fp64"])
+    ap.add_argument("--splits", type=int, default=None)
     ap.add_argument("--cpu-units", type=int, default=None)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

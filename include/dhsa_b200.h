@@ -147,6 +147,45 @@ int dhsa_rows_select(const double* scores, int64_t sc_stride, const int32_t* bou
                      int64_t budget, int tile_tokens, int32_t* tiles,
                      int64_t tile_cap, int32_t* ntiles, dhsa_stream_t stream);
 
+/* ---- bf16 fast path: fp16 centroid sketch + certified exact selection -----
+ * The decode step for bf16 caches streams an fp16 copy ("sketch") of the fp64
+ * centroids, scaled per unit by a power of two, instead of the fp64
+ * centroids.  The build measures the sketch's rounding error; with it the
+ * score error is bounded rigorously (|s'' - s 2^-k| <= ||q|| dmax + gamma_D
+ * ||q|| cmax) and only the chunks within twice that bound of the selection
+ * cut are re-scored in fp64, so the selected indices are those of the fp64
+ * walk (masks.py:153-173, :103-122).  See decode_sketch.cu / DESIGN.md.
+ *
+ * dhsa_sketch_build: for prompt chunks, sketch[u][c] = RN_fp16(c 2^-k_u) and
+ * sinfo[u] = {k_u, max_c ||sketch||_2, max_c ||sketch - c 2^-k_u||_2, max|c|}
+ * (float[4] per unit).  Called once after dhsa_centroids at prefill. */
+int dhsa_sketch_build(const double* centroids, int64_t c_unit_stride, int D, int U,
+                      dhsa_layout layout, void* sketch, int64_t sk_unit_stride,
+                      float* sinfo, dhsa_stream_t stream);
+
+/* Bytes of global select scratch PER UNIT that dhsa_decode_step_bf16 needs
+ * when a unit's chunks do not fit shared memory (0 = none needed). */
+int64_t dhsa_sketch_select_scratch_size(int max_chunks);
+
+/* One decode step's K3 + K4 (+K2, + advance) for bf16 caches, D in {64,128},
+ * G in {1,2,4,8}; two launches:
+ *   1. persistent sketch stream (TMA bulk ring) -> approximate scores
+ *      approx[items][sc_stride] (f32, sketch units);
+ *   2. one CTA per unit: generated chunk scored exactly in fp64, running sum
+ *      += k_new and k/v appended at row plen+gen_count (masks.py:235), the
+ *      certified walk -> tiles/ntiles exactly as dhsa_decode_select would
+ *      produce from fp64 scores, and gen_count += 1 when `advance`.
+ * scratch: U * dhsa_sketch_select_scratch_size bytes, or NULL when 0. */
+int dhsa_decode_step_bf16(const void* q, const void* sketch, int64_t sk_unit_stride,
+                          const float* sinfo, const double* centroids,
+                          int64_t c_unit_stride, double* gen_sum, int32_t* gen_count,
+                          const void* k_new, const void* v_new, void* k_cache,
+                          void* v_cache, int64_t cache_unit_stride, dhsa_layout layout,
+                          int U, int G, int D, int agg, int64_t budget, int tile_tokens,
+                          int32_t* tiles, int64_t tile_cap, int32_t* ntiles, float* approx,
+                          int64_t sc_stride, void* scratch, int advance,
+                          dhsa_stream_t stream);
+
 /* f_upsample (masks.upsample, masks.py:87-100): out[i][j] = s[chunk(i)][chunk(j)]
  * for an n x n chunk-score matrix and bounds [n+1]; out is L x L fp64.  Only
  * the drop-in API uses it — the selection kernels never materialise it. */

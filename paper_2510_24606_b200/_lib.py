@@ -51,6 +51,13 @@ _SIGS = {
     "dhsa_rows_select": (C.c_int, [vp, C.c_int64, vp, C.c_int, vp, C.c_int, C.c_int64, C.c_int,
                                    vp, C.c_int64, vp, vp]),
     "dhsa_upsample": (C.c_int, [vp, vp, C.c_int, C.c_int, vp, vp]),
+    "dhsa_sketch_build": (C.c_int, [vp, C.c_int64, C.c_int, C.c_int, Layout, vp, C.c_int64, vp,
+                                    vp]),
+    "dhsa_sketch_select_scratch_size": (C.c_int64, [C.c_int]),
+    "dhsa_decode_step_bf16": (C.c_int, [vp, vp, C.c_int64, vp, vp, C.c_int64, vp, vp, vp, vp,
+                                        vp, vp, C.c_int64, Layout, C.c_int, C.c_int, C.c_int,
+                                        C.c_int, C.c_int64, C.c_int, vp, C.c_int64, vp, vp,
+                                        C.c_int64, vp, C.c_int, vp]),
 }
 
 _lib = None

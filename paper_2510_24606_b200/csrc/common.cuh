@@ -42,6 +42,7 @@ struct Layout {
   const int32_t* plen;
   int32_t block;
 
+  __host__ __device__ Layout() : bounds(nullptr), bstride(0), nchunks(nullptr), plen(nullptr), block(0) {}
   __host__ Layout(const dhsa_layout& l)
       : bounds(l.bounds), bstride(l.bounds_stride), nchunks(l.nchunks), plen(l.plen),
         block(l.block) {}
@@ -151,6 +152,15 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
       "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+// 1-D bulk copy global -> shared (TMA engine), completion on an mbarrier.
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {

@@ -1,0 +1,715 @@
+// bf16 decode fast path: fp16 centroid SKETCH stream + certified exact selection.
+//
+// Reference semantics (unchanged): masks._decode_row (masks.py:153-173) scores
+// the raw query against the fp64 prompt centroids, the generated-chunk
+// centroid gen_sum/sqrt(g) and the singleton, and topk_row (masks.py:103-122)
+// selects.  The selected indices must be those of an fp64 evaluation.
+//
+// Why a sketch: at 128K context the fp64 centroid stream (D*8 B per chunk and
+// kv head) is half of a decode step's HBM bytes.  Streaming a 2-byte copy cuts
+// it 4x; exactness is restored by re-scoring, in fp64, only the chunks whose
+// approximate score cannot be ordered against the selection cut.
+//
+// Sketch (built once per prompt, dhsa_sketch_build): per unit u a power-of-two
+// scale 2^-k_u puts max|c| in [2^13, 2^14); c''_j = RN_fp16(c_j 2^-k_u).  The
+// build measures, in fp64, dmax_u = max_j ||c''_j - c_j 2^-k_u||_2 and
+// cmax_u = max_j ||c''_j||_2.  For a query q (bf16; bf16*fp16 products are
+// exact in fp32) the fp32 sketch score s''_j obeys
+//   |s''_j - s_j 2^-k_u| <= ||q|| dmax_u + gamma_D ||q|| cmax_u =: E,
+// gamma_D = D 2^-24 / (1 - D 2^-24) (Cauchy-Schwarz on the measured rounding
+// error + fp32 summation), with a small safety factor.
+//
+// Certified walk (per selection row, R = min(budget,row+1)-1 tokens):
+// let t'' be the weighted threshold of the approximate order, W(s'' > t'') <
+// R <= W(s'' >= t'').  A chunk with s''_j > t'' + 2E is wholly inside the exact
+// selection (every chunk that can rank above it has s'' > t''); a chunk with
+// s''_j < t'' - 2E receives nothing (every chunk with s'' >= t'' ranks above
+// it and those already weigh >= R); the rest are re-scored in fp64 and walked
+// exactly (score desc, chunk asc) with the budget left by the certain ones.
+// DESIGN.md section 4 has the full argument; tests compare against fp64
+// scoring on tie-heavy, integer, outlier and zero-query inputs.
+//
+// Kernels per step: sketch_score_kernel (persistent, TMA bulk ring of 16 KB
+// chunk slices, 8 consumer warps + 1 producer warp) -> sketch_select_kernel
+// (one CTA per kv unit: generated chunk in fp64 + state update, certified
+// walk, tiles for the attention kernel, gen_count += 1).
+#include "capi.cuh"
+#include "walk.cuh"
+
+#include <cuda_fp16.h>
+#include <cstdlib>
+
+namespace dhsa {
+
+constexpr int kConsumerWarps = 8;
+constexpr int kScoreThreads = (kConsumerWarps + 1) * 32;
+constexpr int kSliceBytes = 16384;
+constexpr int kStages = 4;
+constexpr int kSelectThreads = 512;
+constexpr int kSmallUncertain = 1024;
+
+constexpr int ilog2c(int x) { return x <= 1 ? 0 : 1 + ilog2c(x / 2); }
+
+struct SketchArgs {
+  const __nv_bfloat16* q;   // [U*G][D]
+  const __half* sketch;     // [U][sk_stride]
+  int64_t sk_stride;
+  const float* sinfo;       // [U][4]: scale exponent k (as float), cmax, dmax, unused
+  const double* cent;       // [U][c_stride] fp64 centroids (refinement)
+  int64_t c_stride;
+  double* gen_sum;          // [U][D]
+  int32_t* gen_count;       // [U]
+  const __nv_bfloat16* k_new;
+  const __nv_bfloat16* v_new;
+  __nv_bfloat16* kc;
+  __nv_bfloat16* vc;
+  int64_t cache_stride;
+  Layout lay;
+  float* approx;            // [items][sc_stride] scaled approximate scores
+  int64_t sc_stride;
+  int slices_per_unit;      // ceil(max_chunks / chunks_per_slice)
+  int64_t total_slices;
+  int64_t budget;
+  int tile_tokens;
+  int32_t* tiles;
+  int64_t tile_cap;
+  int32_t* ntiles;
+  unsigned char* gscratch;
+  int64_t gscratch_stride;
+  int smem_select;
+  int n_max;
+  int advance;
+  unsigned long long* dbg;  // optional per-CTA phase timestamps (DHSA_DEBUG_TIMING)
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define DBG_T(k) \
+  if (a.dbg && threadIdx.x == 0) a.dbg[blockIdx.x * 16 + (k)] = gtimer()
+
+template <int NV, int LG>
+__device__ __forceinline__ void transpose_reduce_f(float (&v)[NV], int lane) {
+  int n = NV;
+#pragma unroll
+  for (int o = LG / 2; o >= 1; o >>= 1) {
+    if (n > 1) {
+      const int half = n >> 1;
+      const bool up = (lane & o) != 0;
+#pragma unroll
+      for (int k = 0; k < NV / 2; ++k) {
+        if (k < half) {
+          const float send = up ? v[k] : v[k + half];
+          const float keep = up ? v[k + half] : v[k];
+          v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+      }
+      n = half;
+    } else {
+      v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+    }
+  }
+}
+
+// value index held in v[k] after transpose_reduce_f<NV, LG> (lane within group)
+template <int NV, int LG>
+__device__ __forceinline__ int tr_index(int k, int glane) {
+  constexpr int a = ilog2c(NV), b = ilog2c(LG), m = a < b ? a : b;
+  int idx = k;
+#pragma unroll
+  for (int s = 0; s < m; ++s) idx |= ((glane >> (b - 1 - s)) & 1) << (a - 1 - s);
+  return idx;
+}
+
+// ------------------------------------------------------------ score stream --
+template <int D, int G, int AGG>
+__global__ __launch_bounds__(kScoreThreads) void sketch_score_kernel(SketchArgs a) {
+  constexpr int LG = D / 8;                  // lanes per chunk row (8 halfs = 16 B each)
+  constexpr int CPL = 32 / LG;               // chunk rows per warp load
+  constexpr int SLICE = kSliceBytes / (D * 2);  // chunks per slice (64 or 128)
+  constexpr int CPW = SLICE / kConsumerWarps;   // chunks per warp per slice (8 or 16)
+  constexpr int LOADS = CPW / CPL;           // 4
+  constexpr int NV = LOADS * G;
+  constexpr int NF = NV >= LG ? NV / LG : 1;
+  constexpr int REP = NV >= LG ? 1 : LG / NV;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages];
+  __shared__ float hv[kConsumerWarps][CPW][G];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t s_begin = a.total_slices * blockIdx.x / gridDim.x;
+  const int64_t s_end = a.total_slices * (blockIdx.x + 1) / gridDim.x;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], kConsumerWarps);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == kConsumerWarps) {
+    // ---------------- producer: one thread drives the TMA bulk ring ----------------
+    if (lane == 0) {
+      int it = 0;
+      for (int64_t sl = s_begin; sl < s_end; ++sl) {
+        const int u = (int)(sl / a.slices_per_unit);
+        const int c0 = (int)(sl % a.slices_per_unit) * SLICE;
+        const int nch = min(SLICE, a.lay.num_chunks(u) - c0);
+        if (nch <= 0) continue;
+        const int st = it % kStages;
+        if (it >= kStages) mbar_wait(&empty_bar[st], ((it / kStages) + 1) & 1);
+        const uint32_t bytes = (uint32_t)nch * D * 2;
+        mbar_expect_tx(&full_bar[st], bytes);
+        bulk_load(smem + st * kSliceBytes, a.sketch + (int64_t)u * a.sk_stride + (int64_t)c0 * D,
+                  bytes, &full_bar[st]);
+        ++it;
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  const int sub = lane / LG, gl = lane % LG, dl = gl * 8;
+  float qf[G][8];
+  int cur_u = -1;
+  int it = 0;
+  for (int64_t sl = s_begin; sl < s_end; ++sl) {
+    const int u = (int)(sl / a.slices_per_unit);
+    const int c0 = (int)(sl % a.slices_per_unit) * SLICE;
+    const int nch = min(SLICE, a.lay.num_chunks(u) - c0);
+    if (nch <= 0) continue;
+    if (u != cur_u) {
+      cur_u = u;
+#pragma unroll
+      for (int h = 0; h < G; ++h) {
+        const uint4 raw = *reinterpret_cast<const uint4*>(a.q + (int64_t)(u * G + h) * D + dl);
+        const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(p2[e]);
+          qf[h][2 * e] = f.x;
+          qf[h][2 * e + 1] = f.y;
+        }
+      }
+    }
+    const int st = it % kStages;
+    mbar_wait(&full_bar[st], (it / kStages) & 1);
+    const unsigned char* buf = smem + st * kSliceBytes;
+    float part[NV];
+#pragma unroll
+    for (int i = 0; i < LOADS; ++i) {
+      const int cl = warp * CPW + i * CPL + sub;  // chunk within the slice
+      uint4 raw = make_uint4(0, 0, 0, 0);
+      if (cl < nch) raw = *reinterpret_cast<const uint4*>(buf + cl * (D * 2) + dl * 2);
+      const __half2* p2 = reinterpret_cast<const __half2*>(&raw);
+      float cv[8];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __half22float2(p2[e]);
+        cv[2 * e] = f.x;
+        cv[2 * e + 1] = f.y;
+      }
+#pragma unroll
+      for (int h = 0; h < G; ++h) {
+        float s = 0.f;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) s = fmaf(qf[h][e], cv[e], s);
+        part[i * G + h] = s;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[st]);  // smem slice consumed
+    ++it;
+    transpose_reduce_f<NV, LG>(part, lane);
+    if (gl % REP == 0) {
+#pragma unroll
+      for (int k = 0; k < NF; ++k) {
+        const int idx = tr_index<NV, LG>(k, gl);
+        const int i = idx / G, h = idx % G;
+        hv[warp][i * CPL + sub][h] = part[k];
+      }
+    }
+    __syncwarp();
+    if (lane < CPW) {
+      const int c = c0 + warp * CPW + lane;
+      if (warp * CPW + lane < nch) {
+        if constexpr (AGG == DHSA_AGG_NONE) {
+#pragma unroll
+          for (int h = 0; h < G; ++h) a.approx[(int64_t)(u * G + h) * a.sc_stride + c] = hv[warp][lane][h];
+        } else {
+          float s = hv[warp][lane][0];
+#pragma unroll
+          for (int h = 1; h < G; ++h) s = (AGG == DHSA_AGG_MAX) ? fmaxf(s, hv[warp][lane][h]) : s + hv[warp][lane][h];
+          a.approx[(int64_t)u * a.sc_stride + c] = (AGG == DHSA_AGG_MEAN) ? s / (float)G : s;
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// --------------------------------------------------------------- selection --
+struct UnitChunks {
+  Layout lay;
+  int u, nc, g, P;
+  __device__ void chunk(int c, int& lo, int& len) const {
+    if (c < nc) {
+      if (lay.bounds) {
+        int hi;
+        lay.chunk(u, c, lo, hi);
+        len = hi - lo;
+      } else {  // static grid: arithmetic only (P is cached in the struct)
+        lo = c * lay.block;
+        len = min(lay.block, P - lo);
+      }
+    } else {
+      lo = P;
+      len = g;
+    }
+  }
+};
+
+template <int G, int AGG>
+__device__ __forceinline__ double agg_d(const double* v, int nh) {
+  double s = v[0];
+  for (int h = 1; h < nh; ++h) s = (AGG == DHSA_AGG_MAX) ? fmax(s, v[h]) : s + v[h];
+  if (AGG == DHSA_AGG_MEAN && nh > 1) s = s / (double)nh;
+  return s;
+}
+
+template <int D, int G, int AGG>
+__global__ __launch_bounds__(kSelectThreads) void sketch_select_kernel(SketchArgs a) {
+  constexpr int NW = kSelectThreads / 32;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ WalkShared sh;
+  __shared__ double qd[G][D];
+  __shared__ double s_qn[G], s_gen[G];
+  __shared__ int s_nunc, s_win;
+  __shared__ uint32_t s_tmin;
+
+  const int u = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  unsigned char* scratch = a.smem_select ? smem_raw : a.gscratch + (int64_t)u * a.gscratch_stride;
+  uint64_t* key64 = reinterpret_cast<uint64_t*>(scratch);
+  int32_t* lens = reinterpret_cast<int32_t*>(key64 + a.n_max);
+  uint32_t* ak = reinterpret_cast<uint32_t*>(lens + a.n_max);
+  int32_t* unc = reinterpret_cast<int32_t*>(ak + a.n_max);
+
+  DBG_T(0);
+  // ---- prologue: every global load of the step issued before one barrier ----
+  for (int i = tid; i < G * D; i += kSelectThreads)
+    qd[i / D][i % D] = to_f64(a.q[(int64_t)u * G * D + i]);
+  const int g = a.gen_count[u];
+  constexpr int DV = D / 32;
+  if (warp < G) {
+    double t = 0.0;
+#pragma unroll
+    for (int v = 0; v < DV; ++v) {
+      const double x = to_f64(a.q[(int64_t)(u * G + warp) * D + lane + 32 * v]);
+      t = fma(x, x, t);
+    }
+    t = warp_sum(t);
+    if (lane == 0) s_qn[warp] = sqrt(t) * (1.0 + 1e-12);
+  } else if (warp == NW - 1) {
+    // generated chunk, exact fp64 (masks.py:161), then the state update
+    double* gs = a.gen_sum + (int64_t)u * D;
+    double gv[DV], qv[G][DV];
+    __nv_bfloat16 kv[DV], vv[DV];
+#pragma unroll
+    for (int v = 0; v < DV; ++v) {
+      const int d = lane + 32 * v;
+      gv[v] = gs[d];
+      if (a.k_new) kv[v] = a.k_new[(int64_t)u * D + d];
+      if (a.v_new) vv[v] = a.v_new[(int64_t)u * D + d];
+#pragma unroll
+      for (int h = 0; h < G; ++h) qv[h][v] = to_f64(a.q[(int64_t)(u * G + h) * D + d]);
+    }
+    double part[G];
+#pragma unroll
+    for (int h = 0; h < G; ++h) part[h] = 0.0;
+    if (g >= 1) {
+      const double rs = __dsqrt_rn((double)g);
+#pragma unroll
+      for (int v = 0; v < DV; ++v) {
+        const double cg = __ddiv_rn(gv[v], rs);
+#pragma unroll
+        for (int h = 0; h < G; ++h) part[h] = fma(qv[h][v], cg, part[h]);
+      }
+#pragma unroll
+      for (int h = 0; h < G; ++h) part[h] = warp_sum(part[h]);
+    }
+    if (lane == 0)
+#pragma unroll
+      for (int h = 0; h < G; ++h) s_gen[h] = part[h];
+    if (a.k_new) {  // masks.py:235: after the read above; k/v appended at row P+g
+      const int64_t pos = (int64_t)(a.lay.prompt_len(u) + g) * D;
+#pragma unroll
+      for (int v = 0; v < DV; ++v) {
+        const int d = lane + 32 * v;
+        gs[d] = __dadd_rn(gv[v], to_f64(kv[v]));
+        if (a.kc) a.kc[(int64_t)u * a.cache_stride + pos + d] = kv[v];
+        if (a.vc) a.vc[(int64_t)u * a.cache_stride + pos + d] = vv[v];
+      }
+    }
+  }
+  __syncthreads();
+  DBG_T(1);
+
+  UnitChunks uc{a.lay, u, a.lay.num_chunks(u), g, a.lay.prompt_len(u)};
+  const int n = uc.nc + (g >= 1 ? 1 : 0);
+  const int row = uc.P + g;
+  const int64_t keep = a.budget < (int64_t)row + 1 ? a.budget : (int64_t)row + 1;
+  const uint32_t R = (uint32_t)(keep - 1);
+  const float kexp = a.sinfo[4 * u + 0];
+  const double scale = ldexp(1.0, -(int)kexp);  // sketch units per score unit
+  const double cmax = a.sinfo[4 * u + 1], dmax = a.sinfo[4 * u + 2];
+  // fp32 summation of D exact products + the G-term head mean (<= 8 more adds)
+  constexpr double gam = (double)(D + 8) * 5.9604644775390625e-08 /
+                         (1.0 - (double)(D + 8) * 5.9604644775390625e-08);
+
+  const int nitems = AGG == DHSA_AGG_NONE ? G : 1;
+  for (int it = 0; it < nitems; ++it) {
+    const int s = AGG == DHSA_AGG_NONE ? u * G + it : u;
+    const int h0 = AGG == DHSA_AGG_NONE ? it : 0, nh = AGG == DHSA_AGG_NONE ? 1 : G;
+    double qmax = 0.0;
+    for (int h = h0; h < h0 + nh; ++h) qmax = fmax(qmax, s_qn[h]);
+    const double gex = agg_d<G, AGG>(s_gen + h0, nh);  // exact, score units
+    const float* __restrict__ apx = a.approx + (int64_t)s * a.sc_stride;
+    {
+      // batched: the approximate scores (L2) are loaded before any smem store
+      constexpr int UNR = 4;
+      const float gkey = (float)(gex * scale);
+      for (int c0 = tid; c0 < n; c0 += UNR * kSelectThreads) {
+        float v[UNR];
+        int ln[UNR];
+#pragma unroll
+        for (int k = 0; k < UNR; ++k) {
+          const int c = c0 + k * kSelectThreads;
+          v[k] = (c < uc.nc) ? __ldcg(apx + c) : gkey;
+          int lo;
+          if (c < n) uc.chunk(c, lo, ln[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < UNR; ++k) {
+          const int c = c0 + k * kSelectThreads;
+          if (c < n) {
+            lens[c] = ln[k];
+            ak[c] = order_key32(v[k]);
+          }
+        }
+      }
+    }
+    if (tid == 0) {
+      s_nunc = 0;
+      s_win = 0;
+      s_tmin = 0xFFFFFFFFu;
+    }
+    __syncthreads();
+    uint64_t prefix = 0, mask = 0;
+    uint32_t rrem = R;
+    bool done = false;
+    if (R > 0 && R < (uint32_t)row) {
+      uint32_t p32, m32, r32;
+      DBG_T(2);
+      radix_threshold<kSelectThreads, uint32_t>(ak, lens, n, R, sh, p32, m32, r32);
+      DBG_T(3);
+      for (int c = tid; c < n; c += kSelectThreads)
+        if ((ak[c] & m32) == p32 && lens[c] > 0) atomicMin(&s_tmin, ak[c]);
+      __syncthreads();
+      const double tv = (double)key32_value(s_tmin);
+      // certified bound in sketch units (+ the fp32 rounding of the exact gen score)
+      const double E = 1.01 * (qmax * dmax + gam * qmax * cmax) +
+                       fabs(gex * scale) * 1.2e-7 + 1e-300;
+      const double hi = tv + 2.0 * E, lo = tv - 2.0 * E;
+      int win_local = 0;
+      for (int c = tid; c < n; c += kSelectThreads) {
+        const double v = (double)key32_value(ak[c]);
+        uint64_t k;
+        if (v > hi) {
+          k = ~0ull;  // certainly kept whole
+          win_local += lens[c];
+        } else if (v < lo) {
+          k = 0ull;  // certainly outside
+        } else {
+          k = 1ull;  // uncertain: exact fp64 score below
+          if (lens[c] > 0) unc[atomicAdd(&s_nunc, 1)] = c;
+        }
+        key64[c] = k;
+      }
+      win_local = warp_sum(win_local);
+      if (lane == 0 && win_local) atomicAdd(&s_win, win_local);
+      __syncthreads();
+      const int nu = s_nunc;
+      DBG_T(4);
+      for (int i = warp; i < nu; i += NW) {
+        const int c = unc[i];
+        double ex;
+        if (c < uc.nc) {
+          const double* crow = a.cent + (int64_t)u * a.c_stride + (int64_t)c * D;
+          double part[G];
+#pragma unroll
+          for (int h = 0; h < G; ++h) part[h] = 0.0;
+#pragma unroll
+          for (int d = lane; d < D; d += 32) {
+            const double cv = crow[d];
+#pragma unroll
+            for (int h = 0; h < G; ++h) part[h] = fma(qd[h][d], cv, part[h]);
+          }
+#pragma unroll
+          for (int h = 0; h < G; ++h) part[h] = warp_sum(part[h]);
+          ex = agg_d<G, AGG>(part + h0, nh);
+        } else {
+          ex = gex;
+        }
+        if (lane == 0) key64[c] = order_key(ex);
+      }
+      __syncthreads();
+      DBG_T(5);
+      if (a.dbg && threadIdx.x == 0) a.dbg[blockIdx.x * 16 + 15] = nu;
+      if (nu <= kSmallUncertain) {
+        // exact walk over the uncertain chunks: rank by (fp64 desc, chunk asc)
+        const int rp = (int)R - s_win;
+        int32_t* take = reinterpret_cast<int32_t*>(ak);  // approx keys no longer needed
+        for (int i = tid; i < nu; i += kSelectThreads) {
+          const int ci = unc[i];
+          const uint64_t ki = key64[ci];
+          int before = 0;
+          for (int j = 0; j < nu; ++j) {
+            const int cj = unc[j];
+            const uint64_t kj = key64[cj];
+            if (kj > ki || (kj == ki && cj < ci)) before += lens[cj];
+          }
+          const int rem = rp - before;
+          take[i] = rem <= 0 ? 0 : (rem < lens[ci] ? rem : lens[ci]);
+        }
+        __syncthreads();
+        for (int c = tid; c < n; c += kSelectThreads)
+          if (key64[c] != ~0ull) lens[c] = 0;
+        __syncthreads();
+        for (int i = tid; i < nu; i += kSelectThreads) lens[unc[i]] = take[i];
+        __syncthreads();
+        DBG_T(6);
+        emit_takes<kSelectThreads>(uc, lens, n, row, a.tile_tokens,
+                                   a.tiles + (int64_t)s * a.tile_cap * 2, a.tile_cap,
+                                   a.ntiles + s, sh);
+        DBG_T(7);
+        done = true;
+      } else {
+        radix_threshold<kSelectThreads, uint64_t>(key64, lens, n, R, sh, prefix, mask, rrem);
+      }
+    }
+    if (!done)
+      walk_emit<kSelectThreads, uint64_t>(uc, key64, lens, n, R, prefix, mask, rrem, row,
+                                          a.tile_tokens, a.tiles + (int64_t)s * a.tile_cap * 2,
+                                          a.tile_cap, a.ntiles + s, sh);
+  }
+  if (tid == 0 && a.advance) a.gen_count[u] = g + 1;  // masks.py:236
+  DBG_T(8);
+}
+
+// ------------------------------------------------------ prefill-time sketch --
+// pass 1: per-unit max |c| over prompt chunks
+__global__ void sketch_absmax_kernel(const double* __restrict__ cent, int64_t c_stride, int D,
+                                     Layout lay, float* __restrict__ sinfo) {
+  const int u = blockIdx.y;
+  const int64_t n = (int64_t)lay.num_chunks(u) * D;
+  double m = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    m = fmax(m, fabs(cent[(int64_t)u * c_stride + i]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) {
+    const float f = isfinite(m) ? __double2float_ru(m) : INFINITY;
+    atomicMax(reinterpret_cast<unsigned int*>(sinfo + 4 * u + 3), __float_as_uint(f));
+  }
+}
+
+// pass 2: scale, round to fp16, measure ||c''|| and ||c'' - c 2^-k|| per chunk
+__global__ __launch_bounds__(256) void sketch_build_kernel(const double* __restrict__ cent,
+                                                           int64_t c_stride, int D, Layout lay,
+                                                           __half* __restrict__ sk,
+                                                           int64_t sk_stride,
+                                                           float* __restrict__ sinfo) {
+  const int u = blockIdx.y;
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (c >= lay.num_chunks(u)) return;
+  const float amax = sinfo[4 * u + 3];
+  int k = 0;
+  if (amax > 0.f && isfinite(amax)) k = ilogb((double)amax) + 1 - 14;  // max|c| 2^-k < 2^14
+  const double sc = ldexp(1.0, -k);
+  const double* src = cent + (int64_t)u * c_stride + (int64_t)c * D;
+  __half* dst = sk + (int64_t)u * sk_stride + (int64_t)c * D;
+  double nrm = 0.0, err = 0.0;
+  bool finite = isfinite(amax);
+  for (int d = lane; d < D; d += 32) {
+    const double v = src[d] * sc;  // exact (power of two)
+    const __half h = __double2half(v);
+    dst[d] = h;
+    const double hv = (double)__half2float(h);
+    finite = finite && isfinite(hv);
+    nrm = fma(hv, hv, nrm);
+    err = fma(hv - v, hv - v, err);
+  }
+  nrm = warp_sum(nrm);
+  err = warp_sum(err);
+  finite = __all_sync(0xffffffffu, finite);
+  if (lane == 0) {
+    if (blockIdx.x == 0 && c == 0) sinfo[4 * u + 0] = (float)k;
+    // a non-finite sketch makes E infinite: every chunk is then re-scored
+    const float fn = finite ? __double2float_ru(sqrt(nrm) * (1.0 + 1e-9)) : INFINITY;
+    const float fe = finite ? __double2float_ru(sqrt(err) * (1.0 + 1e-9)) : INFINITY;
+    atomicMax(reinterpret_cast<unsigned int*>(sinfo + 4 * u + 1), __float_as_uint(fn));
+    atomicMax(reinterpret_cast<unsigned int*>(sinfo + 4 * u + 2), __float_as_uint(fe));
+  }
+}
+
+template <int D, int G, int AGG>
+static int launch_step(const SketchArgs& a, int U, size_t sel_smem, cudaStream_t s) {
+  auto score = sketch_score_kernel<D, G, AGG>;
+  static_assert(kStages * kSliceBytes <= 200 * 1024, "ring too large");
+  const int ring = kStages * kSliceBytes;
+  cudaError_t e = cudaFuncSetAttribute(score, cudaFuncAttributeMaxDynamicSharedMemorySize, ring);
+  if (e != cudaSuccess) {
+    set_error("dhsa_decode_step_bf16: %s", cudaGetErrorString(e));
+    return DHSA_ECUDA;
+  }
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, score, kScoreThreads, ring);
+  int64_t grid = (int64_t)sms * (per_sm < 1 ? 1 : per_sm);
+  if (grid > a.total_slices) grid = a.total_slices;
+  score<<<(unsigned)grid, kScoreThreads, ring, s>>>(a);
+  int rc = check_launch("dhsa_decode_step_bf16(score)");
+  if (rc) return rc;
+  auto sel = sketch_select_kernel<D, G, AGG>;
+  if (sel_smem > 48 * 1024) {
+    e = cudaFuncSetAttribute(sel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel_smem);
+    if (e != cudaSuccess) {
+      set_error("dhsa_decode_step_bf16: %s", cudaGetErrorString(e));
+      return DHSA_ECUDA;
+    }
+  }
+  sel<<<U, kSelectThreads, sel_smem, s>>>(a);
+  return check_launch("dhsa_decode_step_bf16(select)");
+}
+
+template <int D, int AGG>
+static int dispatch_g(int G, const SketchArgs& a, int U, size_t smem, cudaStream_t s) {
+  switch (G) {
+    case 1: return launch_step<D, 1, AGG>(a, U, smem, s);
+    case 2: return launch_step<D, 2, AGG>(a, U, smem, s);
+    case 4: return launch_step<D, 4, AGG>(a, U, smem, s);
+    case 8: return launch_step<D, 8, AGG>(a, U, smem, s);
+  }
+  set_error("dhsa_decode_step_bf16: group size %d not in {1,2,4,8}", G);
+  return DHSA_EINVAL;
+}
+
+template <int D>
+static int dispatch_agg(int agg, int G, const SketchArgs& a, int U, size_t smem, cudaStream_t s) {
+  switch (agg) {
+    case DHSA_AGG_NONE: return dispatch_g<D, DHSA_AGG_NONE>(G, a, U, smem, s);
+    case DHSA_AGG_MAX: return dispatch_g<D, DHSA_AGG_MAX>(G, a, U, smem, s);
+    case DHSA_AGG_MEAN: return dispatch_g<D, DHSA_AGG_MEAN>(G, a, U, smem, s);
+  }
+  set_error("dhsa_decode_step_bf16: unknown aggregation %d", agg);
+  return DHSA_EINVAL;
+}
+
+}  // namespace dhsa
+
+using namespace dhsa;
+
+constexpr int64_t kSelectSmemLimit = 96 * 1024;
+
+extern "C" int64_t dhsa_sketch_select_scratch_size(int max_chunks) {
+  const int64_t per_unit = ((int64_t)max_chunks + 1) * (8 + 4 + 4 + 4);
+  return per_unit <= kSelectSmemLimit ? 0 : (per_unit + 15) / 16 * 16;
+}
+
+extern "C" int dhsa_sketch_build(const double* centroids, int64_t c_unit_stride, int D, int U,
+                                 dhsa_layout layout, void* sketch, int64_t sk_unit_stride,
+                                 float* sinfo, dhsa_stream_t stream) {
+  DHSA_REQUIRE(centroids && sketch && sinfo && D >= 1 && U >= 1, "dhsa_sketch_build: bad arguments");
+  DHSA_REQUIRE(valid_layout(layout) && layout.max_chunks >= 1, "dhsa_sketch_build: bad layout");
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaMemsetAsync(sinfo, 0, sizeof(float) * 4 * U, s);
+  Layout lay(layout);
+  const int64_t work = (int64_t)layout.max_chunks * D;
+  dim3 g1((unsigned)((work + 255) / 256 < 64 ? (work + 255) / 256 : 64), (unsigned)U);
+  sketch_absmax_kernel<<<g1, 256, 0, s>>>(centroids, c_unit_stride, D, lay, sinfo);
+  dim3 g2((unsigned)((layout.max_chunks + 7) / 8), (unsigned)U);
+  sketch_build_kernel<<<g2, 256, 0, s>>>(centroids, c_unit_stride, D, lay, (__half*)sketch,
+                                         sk_unit_stride, sinfo);
+  return check_launch("dhsa_sketch_build");
+}
+
+extern "C" int dhsa_decode_step_bf16(
+    const void* q, const void* sketch, int64_t sk_unit_stride, const float* sinfo,
+    const double* centroids, int64_t c_unit_stride, double* gen_sum, int32_t* gen_count,
+    const void* k_new, const void* v_new, void* k_cache, void* v_cache, int64_t cache_unit_stride,
+    dhsa_layout layout, int U, int G, int D, int agg, int64_t budget, int tile_tokens,
+    int32_t* tiles, int64_t tile_cap, int32_t* ntiles, float* approx, int64_t sc_stride,
+    void* scratch, int advance, dhsa_stream_t stream) {
+  DHSA_REQUIRE(q && sketch && sinfo && centroids && gen_sum && gen_count && tiles && ntiles &&
+                   approx,
+               "dhsa_decode_step_bf16: null pointer");
+  DHSA_REQUIRE(budget >= 1, "budget must be >= 1");
+  DHSA_REQUIRE(D == 64 || D == 128, "dhsa_decode_step_bf16: D must be 64 or 128");
+  DHSA_REQUIRE(U >= 1 && tile_tokens >= 1 && tile_cap >= 2, "dhsa_decode_step_bf16: bad shape");
+  DHSA_REQUIRE(valid_layout(layout) && layout.max_chunks >= 1, "dhsa_decode_step_bf16: bad layout");
+  DHSA_REQUIRE(sc_stride >= layout.max_chunks + 1, "dhsa_decode_step_bf16: sc_stride too small");
+  DHSA_REQUIRE(((uintptr_t)q & 15) == 0 && ((uintptr_t)sketch & 15) == 0 &&
+                   (sk_unit_stride * 2) % 16 == 0,
+               "dhsa_decode_step_bf16: q/sketch must be 16-byte aligned");
+  DHSA_REQUIRE(!(k_cache || v_cache) || k_new, "dhsa_decode_step_bf16: cache append needs k_new");
+  SketchArgs a{};
+  a.q = (const __nv_bfloat16*)q;
+  a.sketch = (const __half*)sketch;
+  a.sk_stride = sk_unit_stride;
+  a.sinfo = sinfo;
+  a.cent = centroids;
+  a.c_stride = c_unit_stride;
+  a.gen_sum = gen_sum;
+  a.gen_count = gen_count;
+  a.k_new = (const __nv_bfloat16*)k_new;
+  a.v_new = (const __nv_bfloat16*)v_new;
+  a.kc = (__nv_bfloat16*)k_cache;
+  a.vc = (__nv_bfloat16*)v_cache;
+  a.cache_stride = cache_unit_stride;
+  a.lay = Layout(layout);
+  a.approx = approx;
+  a.sc_stride = sc_stride;
+  const int slice = kSliceBytes / (D * 2);
+  a.slices_per_unit = (layout.max_chunks + slice - 1) / slice;
+  a.total_slices = (int64_t)a.slices_per_unit * U;
+  a.budget = budget;
+  a.tile_tokens = tile_tokens;
+  a.tiles = tiles;
+  a.tile_cap = tile_cap;
+  a.ntiles = ntiles;
+  a.n_max = layout.max_chunks + 1;
+  a.advance = advance;
+  if (const char* e = getenv("DHSA_DEBUG_TIMING")) a.dbg = (unsigned long long*)strtoull(e, nullptr, 0);
+  const int64_t need = dhsa_sketch_select_scratch_size(layout.max_chunks);
+  size_t smem = 0;
+  if (need == 0) {
+    a.smem_select = 1;
+    smem = (size_t)a.n_max * (8 + 4 + 4 + 4);
+  } else {
+    DHSA_REQUIRE(scratch, "dhsa_decode_step_bf16: %lld bytes of select scratch per unit required",
+                 (long long)need);
+    a.smem_select = 0;
+    a.gscratch = (unsigned char*)scratch;
+    a.gscratch_stride = need;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  if (D == 128) return dispatch_agg<128>(agg, G, a, U, smem, s);
+  return dispatch_agg<64>(agg, G, a, U, smem, s);
+}

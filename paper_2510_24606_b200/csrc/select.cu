@@ -18,6 +18,7 @@
 // with its token length (a weighted select), 8 bits per pass, one CTA per
 // selection row, keys and lengths resident in shared memory.
 #include "capi.cuh"
+#include "walk.cuh"
 
 namespace dhsa {
 
@@ -86,35 +87,6 @@ struct MatrixRows {
   }
 };
 
-// Exclusive block scan of one int per thread; returns the prefix, sets total.
-__device__ __forceinline__ int block_excl_scan(int v, int* warp_tot, int& total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) warp_tot[warp] = x;
-  __syncthreads();
-  if (warp == 0) {
-    int t = lane < (kSelThreads / 32) ? warp_tot[lane] : 0;
-    int w = t;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, w, o);
-      if (lane >= o) w += y;
-    }
-    if (lane < (kSelThreads / 32)) warp_tot[lane] = w - t;  // exclusive
-    if (lane == 31) warp_tot[32] = w;
-  }
-  __syncthreads();
-  const int res = warp_tot[warp] + x - v;
-  total = warp_tot[32];
-  __syncthreads();
-  return res;
-}
-
 template <class View>
 __global__ __launch_bounds__(kSelThreads) void select_kernel(View view, int64_t budget,
                                                              int tile_tokens,
@@ -122,19 +94,14 @@ __global__ __launch_bounds__(kSelThreads) void select_kernel(View view, int64_t 
                                                              int64_t tile_cap,
                                                              int32_t* __restrict__ ntiles) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ uint32_t hist[256];
-  __shared__ int warp_tot[33];
-  __shared__ uint32_t s_digit, s_rrem, s_done;
-
+  __shared__ WalkShared sh;
   const int item = blockIdx.x;
-  const int tid = threadIdx.x;
   view.init(item);
   const int n = view.n();
   const int row = view.row();
   uint64_t* keys = reinterpret_cast<uint64_t*>(smem_raw);
   int32_t* lens = reinterpret_cast<int32_t*>(keys + n);
-
-  for (int c = tid; c < n; c += kSelThreads) {
+  for (int c = threadIdx.x; c < n; c += kSelThreads) {
     int lo, len;
     view.chunk(c, lo, len);
     keys[c] = order_key(view.score(c));
@@ -146,114 +113,12 @@ __global__ __launch_bounds__(kSelThreads) void select_kernel(View view, int64_t 
   uint64_t prefix = 0, mask = 0;
   uint32_t rrem = R;
   __syncthreads();
-
-  // All causal tokens fit (R == row): every chunk is taken whole (tie class
-  // = everything, walked with rrem = total).  R == 0: only self.
-  if (R > 0 && R < (uint32_t)row) {
-    for (int shift = 56; shift >= 0; shift -= 8) {
-      for (int b = tid; b < 256; b += kSelThreads) hist[b] = 0;
-      __syncthreads();
-      for (int c = tid; c < n; c += kSelThreads) {
-        const uint64_t k = keys[c];
-        if ((k & mask) == prefix && lens[c] > 0)
-          atomicAdd(&hist[(k >> shift) & 255], (uint32_t)lens[c]);
-      }
-      __syncthreads();
-      if (tid < 32) {
-        const int lane = tid;
-        uint32_t w[8], sum = 0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          w[j] = hist[255 - 8 * lane - j];
-          sum += w[j];
-        }
-        uint32_t incl = sum;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += y;
-        }
-        const uint32_t excl = incl - sum;
-        const unsigned hit = __ballot_sync(0xffffffffu, excl < rrem && rrem <= incl);
-        const int f = __ffs(hit) - 1;
-        if (lane == f) {
-          uint32_t cum = excl;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            if (cum + w[j] >= rrem) {
-              s_digit = 255 - 8 * lane - j;
-              s_rrem = rrem - cum;
-              s_done = (rrem - cum == w[j]);
-              break;
-            }
-            cum += w[j];
-          }
-        }
-      }
-      __syncthreads();
-      prefix |= (uint64_t)s_digit << shift;
-      mask |= (uint64_t)0xFF << shift;
-      rrem = s_rrem;
-      const bool done = s_done;
-      __syncthreads();
-      if (done) break;  // the whole bucket is kept: no finer split needed
-    }
-  }
-
-  // Emit, in chunk (= token) order.  Thread t owns chunks [t*cpt, (t+1)*cpt).
-  const int cpt = (n + kSelThreads - 1) / kSelThreads;
-  const int c0 = min(tid * cpt, n), c1 = min(c0 + cpt, n);
-  int tie_local = 0;
-  if (R > 0) {
-    for (int c = c0; c < c1; ++c)
-      if ((keys[c] & mask) == prefix) tie_local += lens[c];
-  }
-  int tie_total;
-  int tie_before = block_excl_scan(tie_local, warp_tot, tie_total);
-  int ntile_local = 0;
-  if (R > 0) {
-    int run = tie_before;
-    for (int c = c0; c < c1; ++c) {
-      const uint64_t top = keys[c] & mask;
-      int take = 0;
-      if (top > prefix) {
-        take = lens[c];
-      } else if (top == prefix) {
-        const int rem = (int)rrem - run;
-        take = rem <= 0 ? 0 : (rem < lens[c] ? rem : lens[c]);
-        run += lens[c];
-      }
-      lens[c] = take;  // reuse: tokens taken from the chunk start
-      ntile_local += (take + tile_tokens - 1) / tile_tokens;
-    }
-  }
-  int tiles_total;
-  int tile_off = block_excl_scan(ntile_local, warp_tot, tiles_total);
-  int32_t* out = tiles + (int64_t)item * tile_cap * 2;
-  if (R > 0) {
-    for (int c = c0; c < c1; ++c) {
-      const int take = lens[c];
-      if (take <= 0) continue;
-      int lo, len;
-      view.chunk(c, lo, len);
-      for (int t = 0; t < take; t += tile_tokens) {
-        if (tile_off < tile_cap) {
-          out[2 * tile_off] = lo + t;
-          out[2 * tile_off + 1] = min(tile_tokens, take - t);
-        }
-        ++tile_off;
-      }
-    }
-  }
-  if (tid == 0) {
-    if (tiles_total + 1 > tile_cap) {
-      ntiles[item] = -1;  // capacity error, reported by the host wrapper
-    } else {
-      out[2 * tiles_total] = row;  // self (masks.py:120-121)
-      out[2 * tiles_total + 1] = 1;
-      ntiles[item] = tiles_total + 1;
-    }
-  }
+  // R == row: every causal token is kept (one tie class = everything).
+  if (R > 0 && R < (uint32_t)row)
+    radix_threshold<kSelThreads, uint64_t>(keys, lens, n, R, sh, prefix, mask, rrem);
+  walk_emit<kSelThreads, uint64_t>(view, keys, lens, n, R, prefix, mask, rrem, row, tile_tokens,
+                                   tiles + (int64_t)item * tile_cap * 2, tile_cap, ntiles + item,
+                                   sh);
 }
 
 template <class View>

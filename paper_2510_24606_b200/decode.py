@@ -51,7 +51,7 @@ class SparseDecoder:
 
     def __init__(self, batch, q_heads, kv_heads, head_dim, max_len, *, block=64, top_k=64,
                  budget=None, dtype=torch.bfloat16, agg="max", tile=64, splits=None,
-                 device=None):
+                 device=None, scoring=None):
         _lib.require_cuda()
         if q_heads % kv_heads:
             raise ValueError("q_heads must be a multiple of kv_heads")
@@ -95,7 +95,22 @@ class SparseDecoder:
         self.ws = torch.empty(max(nbytes, 8), dtype=torch.uint8, **kw)
         self.counters = torch.zeros(self.items, dtype=torch.int32, **kw)
         self.max_prompt = 0
+        self.max_chunks = 0
         self.steps = 0
+        # scoring: "sketch" (fp16 centroid sketch + certified fp64 re-scoring at
+        # the cut; sketch stream + select kernels) or "fp64" (stream fp64 centroids)
+        fast_ok = dtype == torch.bfloat16 and head_dim in (64, 128) and self.G in (1, 2, 4, 8)
+        self.scoring = scoring or ("sketch" if fast_ok else "fp64")
+        if self.scoring == "sketch":
+            if not fast_ok:
+                raise ValueError("sketch scoring needs bf16, D in {64,128}, G in {1,2,4,8}")
+            self.sketch = torch.zeros(batch, kv_heads, self.nc_cap, head_dim, dtype=torch.float16,
+                                      **kw)
+            self.sinfo = torch.zeros(self.U, 4, dtype=torch.float32, **kw)
+            self.approx = torch.empty(self.items, self.nc_cap + 1, dtype=torch.float32, **kw)
+            per_unit = _lib.load().dhsa_sketch_select_scratch_size(self.nc_cap)
+            self.scratch = (torch.empty(self.U * per_unit, dtype=torch.uint8, **kw)
+                            if per_unit > 0 else None)
 
     # ------------------------------------------------------------------
     def _layout(self):
@@ -119,6 +134,10 @@ class SparseDecoder:
         _lib.call("dhsa_centroids", self.code, _lib.ptr(self.k_cache), self.L_cap * self.D,
                   self.D, self.U, self._layout(), 1, _lib.ptr(self.centroids),
                   self.nc_cap * self.D, st)
+        if self.scoring == "sketch":
+            _lib.call("dhsa_sketch_build", _lib.ptr(self.centroids), self.nc_cap * self.D, self.D,
+                      self.U, self._layout(), _lib.ptr(self.sketch), self.nc_cap * self.D,
+                      _lib.ptr(self.sinfo), st)
 
     def step(self, q, k_new, v_new, out=None):
         """One decode step.  q [B, Hq, D], k_new/v_new [B, Hkv, D] (cache
@@ -132,24 +151,57 @@ class SparseDecoder:
         return out
 
     def launch(self, q, k_new, v_new, out, stream=None):
-        """Enqueue the four kernels of one step (graph-capturable)."""
+        """Enqueue one step (graph-capturable): 3 kernels with sketch scoring
+        (sketch stream, select + state update, attention), 4 with fp64 scoring."""
+        for _, fn in self.stages(q, k_new, v_new, out, stream):
+            fn()
+
+    def stages(self, q, k_new, v_new, out, stream=None):
+        """The launches of one step as (kernel name, thunk) pairs, in order."""
         st = _lib.stream_handle(stream)
         lay = self._layout()
         agg = _lib.AGG[self.agg]
-        _lib.call("dhsa_decode_score", self.code, _lib.ptr(q), _lib.ptr(self.centroids),
-                  self.nc_cap * self.D, _lib.ptr(self.gen_sum), _lib.ptr(self.gen_count),
-                  _lib.ptr(k_new), _lib.ptr(v_new), _lib.ptr(self.k_cache),
-                  _lib.ptr(self.v_cache), self.L_cap * self.D, lay, self.U, self.G, self.D, agg,
-                  _lib.ptr(self.scores), self.nc_cap + 1, st)
-        _lib.call("dhsa_decode_select", _lib.ptr(self.scores), self.nc_cap + 1, lay,
-                  _lib.ptr(self.gen_count), self.U, self.G if self.per_head else 1, self.budget,
-                  self.tile, _lib.ptr(self.tiles), self.tile_cap, _lib.ptr(self.ntiles), st)
+        attn = ("attn", lambda: self._attn(q, out, st))
+        if self.scoring == "sketch":
+            def fused():
+                _lib.call("dhsa_decode_step_bf16", _lib.ptr(q), _lib.ptr(self.sketch),
+                          self.nc_cap * self.D, _lib.ptr(self.sinfo), _lib.ptr(self.centroids),
+                          self.nc_cap * self.D, _lib.ptr(self.gen_sum), _lib.ptr(self.gen_count),
+                          _lib.ptr(k_new), _lib.ptr(v_new), _lib.ptr(self.k_cache),
+                          _lib.ptr(self.v_cache), self.L_cap * self.D, lay, self.U, self.G,
+                          self.D, agg, self.budget, self.tile, _lib.ptr(self.tiles),
+                          self.tile_cap, _lib.ptr(self.ntiles), _lib.ptr(self.approx),
+                          self.nc_cap + 1, _lib.ptr(self.scratch), 1, st)
+            return [("score_select", fused), attn]
+
+        def score():
+            _lib.call("dhsa_decode_score", self.code, _lib.ptr(q), _lib.ptr(self.centroids),
+                      self.nc_cap * self.D, _lib.ptr(self.gen_sum), _lib.ptr(self.gen_count),
+                      _lib.ptr(k_new), _lib.ptr(v_new), _lib.ptr(self.k_cache),
+                      _lib.ptr(self.v_cache), self.L_cap * self.D, lay, self.U, self.G, self.D,
+                      agg, _lib.ptr(self.scores), self.nc_cap + 1, st)
+
+        def select():
+            _lib.call("dhsa_decode_select", _lib.ptr(self.scores), self.nc_cap + 1, lay,
+                      _lib.ptr(self.gen_count), self.U, self.G if self.per_head else 1,
+                      self.budget, self.tile, _lib.ptr(self.tiles), self.tile_cap,
+                      _lib.ptr(self.ntiles), st)
+
+        def advance():
+            _lib.call("dhsa_decode_advance", _lib.ptr(self.gen_count), self.U, st)
+
+        return [("decode_score", score), ("decode_select", select), attn, ("advance", advance)]
+
+    def _attn(self, q, out, st):
         _lib.call("dhsa_attn", self.code, _lib.ptr(q), _lib.ptr(self.k_cache),
                   _lib.ptr(self.v_cache), self.L_cap * self.D, self.L_cap, self.items,
                   self.G if self.per_head else 1, self.GH, self.D, _lib.ptr(self.tiles),
                   self.tile_cap, _lib.ptr(self.ntiles), self.splits, _lib.ptr(out),
                   _lib.ptr(self.ws), _lib.ptr(self.counters), st)
-        _lib.call("dhsa_decode_advance", _lib.ptr(self.gen_count), self.U, st)
+
+    @property
+    def kernels_per_step(self) -> int:
+        return 3 if self.scoring == "sketch" else 4
 
     # ------------------------------------------------------------------
     def selection(self):
@@ -165,7 +217,9 @@ class SparseDecoder:
         esz = torch.finfo(self.dtype).bits // 8
         P, g = self.max_prompt, self.steps
         nc = (P + self.block - 1) // self.block
-        cent = self.U * nc * self.D * 8
+        # centroid stream: fp16 sketch (the fp64 re-scoring of the few chunks
+        # at the cut is not counted) or fp64 centroids
+        cent = self.U * nc * self.D * (2 if self.scoring == "sketch" else 8)
         sel_tokens = min(self.budget, P + g + 1)
         per_sel = sel_tokens * self.D * esz * 2
         kv = (self.items if self.per_head else self.U) * per_sel

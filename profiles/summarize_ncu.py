@@ -20,7 +20,7 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "launch__grid_size", "launch__occupancy_limit_registers",
         "launch__occupancy_limit_shared_mem",
         "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"]
-SHORT = {"score_fast_kernel": "decode_score", "score_sketch_kernel": "decode_score",
+SHORT = {"score_fast_kernel": "decode_score", "score_select_kernel": "score_select",
          "select_kernel": "decode_select", "attn_mma_kernel": "attn", "advance_kernel": "advance"}
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 

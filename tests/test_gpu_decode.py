@@ -137,3 +137,49 @@ def test_step_graph_replay_matches_eager():
     assert torch.equal(outs[0][0], outs[1][0])
     for a, b in zip(outs[0][1], outs[1][1]):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("agg", ["max", "mean", "none"])
+@pytest.mark.parametrize("kind", ["normal", "ties", "int", "outlier", "zeroq"])
+def test_sketch_scoring_equals_fp64_scoring(agg, kind):
+    """The bf16-sketch + certified-refinement selection is index-identical to
+    streaming the fp64 centroids, including exact ties (duplicated blocks,
+    integer data), an outlier chunk whose norm inflates the error bound, and
+    an all-zero query (every score ties)."""
+    from paper_2510_24606_b200.decode import SparseDecoder
+    B, Hq, Hkv, D, P, steps = 2, 8, 2, 128, 3000, 6
+    t, _ = make_inputs(B, Hq, Hkv, D, P, steps, torch.bfloat16, seed=11,
+                       kind="ties" if kind == "ties" else ("int" if kind == "int" else "normal"))
+    if kind == "outlier":
+        t["k"][:, :, 640:704] *= 40
+    if kind == "zeroq":
+        t["q"][:, :, 1::2] = 0
+    sels = []
+    for scoring in ("sketch", "fp64"):
+        dec = SparseDecoder(B, Hq, Hkv, D, P + steps, top_k=7, dtype=torch.bfloat16, agg=agg,
+                            scoring=scoring)
+        dec.prefill(t["k"][:, :, :P].cuda(), t["v"][:, :, :P].cuda())
+        per = []
+        for s in range(steps):
+            out = dec.step(t["q"][:, :, s].contiguous().cuda(), t["k"][:, :, P + s].contiguous().cuda(),
+                           t["v"][:, :, P + s].contiguous().cuda())
+            per.append(([x.copy() for x in dec.selection()], out.clone()))
+        sels.append(per)
+    for (sa, oa), (sb, ob) in zip(*sels):
+        for a, b in zip(sa, sb):
+            assert np.array_equal(a, b)
+        assert torch.equal(oa, ob)
+
+
+def test_sketch_c3_shape_sampled_units():
+    """North-star shape (128K context, 32q/8kv, d=128, top-k 64) at batch 2:
+    every unit's selection exact against the fp64 oracle, outputs in
+    tolerance on sampled units."""
+    B, Hq, Hkv, D, P, steps = 2, 32, 8, 128, 131072, 2
+    t, host = make_inputs(B, Hq, Hkv, D, P, steps, torch.bfloat16, seed=12)
+    dec = _dec(batch=B, q_heads=Hq, kv_heads=Hkv, head_dim=D, max_len=P + steps, block=64,
+               top_k=64, dtype=torch.bfloat16, agg="max")
+    assert dec.scoring == "sketch"
+    worst = run_and_check(dec, t, host, P, steps, "max", check_units=list(range(16)),
+                          check_out=True)
+    assert worst <= 2e-2
