@@ -117,13 +117,18 @@ int dhsa_decode_select(const double* scores, int64_t sc_stride, dhsa_layout layo
  * accumulation in the input precision, any D.
  * out: [items*GH][D] in the input dtype (bf16 output for bf16).
  * workspace: dhsa_attn_workspace_size bytes; counters: int32[items], zeroed
- * once by the caller (the kernel re-arms them). */
+ * once by the caller (the kernel re-arms them).
+ * ready (bf16 only, may be NULL): int32[items] flags published by
+ * dhsa_decode_step_bf16; when given, the kernel is launched with programmatic
+ * stream serialization so it overlaps the selection, each CTA waits for its
+ * item's flag, and the last CTA of an item clears it. */
 int64_t dhsa_attn_workspace_size(int dtype, int items, int GH, int D, int splits);
 int dhsa_attn(int dtype, const void* q, const void* k_cache, const void* v_cache,
               int64_t cache_unit_stride, int64_t cache_rows, int items,
               int items_per_unit, int GH, int D, const int32_t* tiles,
               int64_t tile_cap, const int32_t* ntiles, int splits, void* out,
-              void* workspace, int32_t* counters, dhsa_stream_t stream);
+              void* workspace, int32_t* counters, int32_t* ready,
+              dhsa_stream_t stream);
 
 /* gen_count[u] += 1 for all units (masks.py:236). */
 int dhsa_decode_advance(int32_t* gen_count, int U, dhsa_stream_t stream);
@@ -175,7 +180,12 @@ int64_t dhsa_sketch_select_scratch_size(int max_chunks);
  *      += k_new and k/v appended at row plen+gen_count (masks.py:235), the
  *      certified walk -> tiles/ntiles exactly as dhsa_decode_select would
  *      produce from fp64 scores, and gen_count += 1 when `advance`.
- * scratch: U * dhsa_sketch_select_scratch_size bytes, or NULL when 0. */
+ * scratch: U * dhsa_sketch_select_scratch_size bytes, or NULL when 0.
+ * The select kernel is launched with programmatic stream serialization: its
+ * prologue (query staging, generated-chunk update) overlaps the sketch stream
+ * and it waits (griddepcontrol.wait) before reading the scores.
+ * ready: int32[items] (or NULL) flags raised when an item's tiles are final,
+ * consumed by dhsa_attn(..., ready, ...). */
 int dhsa_decode_step_bf16(const void* q, const void* sketch, int64_t sk_unit_stride,
                           const float* sinfo, const double* centroids,
                           int64_t c_unit_stride, double* gen_sum, int32_t* gen_count,
@@ -183,7 +193,7 @@ int dhsa_decode_step_bf16(const void* q, const void* sketch, int64_t sk_unit_str
                           void* v_cache, int64_t cache_unit_stride, dhsa_layout layout,
                           int U, int G, int D, int agg, int64_t budget, int tile_tokens,
                           int32_t* tiles, int64_t tile_cap, int32_t* ntiles, float* approx,
-                          int64_t sc_stride, void* scratch, int advance,
+                          int64_t sc_stride, void* scratch, int32_t* ready, int advance,
                           dhsa_stream_t stream);
 
 /* f_upsample (masks.upsample, masks.py:87-100): out[i][j] = s[chunk(i)][chunk(j)]

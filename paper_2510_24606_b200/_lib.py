@@ -44,7 +44,7 @@ _SIGS = {
                                      C.c_int, vp, C.c_int64, vp, vp]),
     "dhsa_attn_workspace_size": (C.c_int64, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]),
     "dhsa_attn": (C.c_int, [C.c_int, vp, vp, vp, C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int,
-                            C.c_int, vp, C.c_int64, vp, C.c_int, vp, vp, vp, vp]),
+                            C.c_int, vp, C.c_int64, vp, C.c_int, vp, vp, vp, vp, vp]),
     "dhsa_decode_advance": (C.c_int, [vp, C.c_int, vp]),
     "dhsa_chunk_scores": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64,
                                     C.c_int64, vp, C.c_int64, vp]),
@@ -57,7 +57,7 @@ _SIGS = {
     "dhsa_decode_step_bf16": (C.c_int, [vp, vp, C.c_int64, vp, vp, C.c_int64, vp, vp, vp, vp,
                                         vp, vp, C.c_int64, Layout, C.c_int, C.c_int, C.c_int,
                                         C.c_int, C.c_int64, C.c_int, vp, C.c_int64, vp, vp,
-                                        C.c_int64, vp, C.c_int, vp]),
+                                        C.c_int64, vp, vp, C.c_int, vp]),
 }
 
 _lib = None

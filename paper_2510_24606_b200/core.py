@@ -111,7 +111,7 @@ def attend_tiles(q, k, v, tiles, ntiles, splits=1):
         cnt = _dev.zeros((L,), dtype=torch.int32)
     _lib.call("dhsa_attn", _lib.F64, _lib.ptr(q), _lib.ptr(k), _lib.ptr(v), L * d, L, L, L, 1, d,
               _lib.ptr(tiles), cap, _lib.ptr(ntiles), splits, _lib.ptr(out), _lib.ptr(ws),
-              _lib.ptr(cnt), _dev.stream())
+              _lib.ptr(cnt), 0, _dev.stream())
     return out
 
 

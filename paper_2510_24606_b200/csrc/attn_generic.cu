@@ -17,7 +17,8 @@ namespace dhsa {
 int attn_mma_bf16(const void* q, const void* k_cache, const void* v_cache,
                   int64_t cache_unit_stride, int64_t cache_rows, int items, int items_per_unit,
                   int GH, int D, const int32_t* tiles, int64_t tile_cap, const int32_t* ntiles,
-                  int splits, void* out, void* ws, int32_t* counters, cudaStream_t s);
+                  int splits, void* out, void* ws, int32_t* counters, int32_t* ready,
+                  cudaStream_t s);
 
 constexpr int kGHMax = 8;
 
@@ -173,12 +174,14 @@ extern "C" int dhsa_attn(int dtype, const void* q, const void* k_cache, const vo
                          int64_t cache_unit_stride, int64_t cache_rows, int items,
                          int items_per_unit, int GH, int D, const int32_t* tiles,
                          int64_t tile_cap, const int32_t* ntiles, int splits, void* out,
-                         void* workspace, int32_t* counters, dhsa_stream_t stream) {
+                         void* workspace, int32_t* counters, int32_t* ready,
+                         dhsa_stream_t stream) {
   DHSA_REQUIRE(q && k_cache && v_cache && tiles && ntiles && out, "dhsa_attn: null pointer");
   DHSA_REQUIRE(items >= 1 && items_per_unit >= 1 && GH >= 1 && GH <= kGHMax && D >= 1 &&
                    D <= 256 && splits >= 1 && tile_cap >= 1,
                "dhsa_attn: bad shape (GH <= 8, D <= 256)");
   DHSA_REQUIRE(splits == 1 || (workspace && counters), "dhsa_attn: split-KV needs workspace");
+  DHSA_REQUIRE(!ready || dtype == DHSA_BF16, "dhsa_attn: ready flags are a bf16-path feature");
   cudaStream_t s = (cudaStream_t)stream;
   switch (dtype) {
     case DHSA_F64:
@@ -190,7 +193,7 @@ extern "C" int dhsa_attn(int dtype, const void* q, const void* k_cache, const vo
     case DHSA_BF16:
       return attn_mma_bf16(q, k_cache, v_cache, cache_unit_stride, cache_rows, items,
                            items_per_unit, GH, D, tiles, tile_cap, ntiles, splits, out, workspace,
-                           counters, s);
+                           counters, ready, s);
   }
   set_error("dhsa_attn: unknown dtype %d", dtype);
   return DHSA_EINVAL;

@@ -20,7 +20,6 @@
 #include "attn_common.cuh"
 #include "capi.cuh"
 
-#include <cudaTypedefs.h>
 
 namespace dhsa {
 
@@ -29,7 +28,8 @@ __global__ __launch_bounds__(160) void attn_mma_kernel(
     const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
     const __nv_bfloat16* __restrict__ q, int64_t cache_rows, int items_per_unit, int GH,
     const int32_t* __restrict__ tiles, int64_t tile_cap, const int32_t* __restrict__ ntiles,
-    int splits, __nv_bfloat16* __restrict__ out, void* ws, int32_t* counters, float scale_log2) {
+    int splits, __nv_bfloat16* __restrict__ out, void* ws, int32_t* counters, float scale_log2,
+    int32_t* ready) {
   constexpr int NB = D / 64;                  // 128-byte column boxes per row
   constexpr int BOX = 64 * 128;               // one box: 64 token rows x 128 B
   constexpr int STAGE_BYTES = 2 * NB * BOX;   // K + V
@@ -45,7 +45,12 @@ __global__ __launch_bounds__(160) void attn_mma_kernel(
   const int item = blockIdx.y, split = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int unit = item / items_per_unit;
-  const int nt_all = ntiles[item];
+  if (ready) {  // launched early (PDL): wait until the selection of this item is published
+    if (threadIdx.x == 0) spin_geq(ready + item, 1);
+    __syncthreads();
+  }
+  // tiles may have been written while this grid was running: read through L2
+  const int nt_all = __ldcg(ntiles + item);
   const int t_begin = (int)((int64_t)nt_all * split / splits);
   const int n = (int)((int64_t)nt_all * (split + 1) / splits) - t_begin;
   const int32_t* tl = tiles + ((int64_t)item * tile_cap + t_begin) * 2;
@@ -73,7 +78,7 @@ __global__ __launch_bounds__(160) void attn_mma_kernel(
       for (int i = 0; i < n; ++i) {
         const int s = i % STAGES;
         if (i >= STAGES) mbar_wait(&empty_bar[s], ((i / STAGES) + 1) & 1);
-        const int row = (int)(row0 + __ldg(tl + 2 * i));
+        const int row = (int)(row0 + __ldcg(tl + 2 * i));
         unsigned char* st = smem + s * STAGE_BYTES;
         mbar_expect_tx(&full_bar[s], STAGE_BYTES);
 #pragma unroll
@@ -105,7 +110,7 @@ __global__ __launch_bounds__(160) void attn_mma_kernel(
     for (int i = 0; i < n; ++i) {
       const int s = i % STAGES;
       mbar_wait(&full_bar[s], (i / STAGES) & 1);
-      const int count = __ldg(tl + 2 * i + 1);
+      const int count = __ldcg(tl + 2 * i + 1);
       if (warp * 16 < count) {
         const uint32_t kb = smem_u32(smem + s * STAGE_BYTES);
         const uint32_t vb = kb + NB * BOX;
@@ -216,50 +221,21 @@ __global__ __launch_bounds__(160) void attn_mma_kernel(
       p[2 + d] = a;
     }
   }
-  if (direct) return;
-  if (split_arrive(counters, item, splits))
+  if (direct) {
+    if (ready && threadIdx.x == 0) ready[item] = 0;  // re-arm for the next step
+    return;
+  }
+  if (split_arrive(counters, item, splits)) {
     merge_partials<__nv_bfloat16, float>(ws, item, splits, GH, D, out);
-}
-
-static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    if (ready && threadIdx.x == 0) ready[item] = 0;  // every sibling CTA is past its wait
   }
-  return fn;
-}
-
-// 2-D view [rows][D] of a bf16 cache; 64 x 64-element boxes, 128B swizzle.
-static int make_map(CUtensorMap* map, const void* base, int64_t rows, int D) {
-  auto enc = get_encode();
-  if (!enc) {
-    set_error("cuTensorMapEncodeTiled unavailable");
-    return DHSA_ECUDA;
-  }
-  cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)D * 2};
-  cuuint32_t box[2] = {64, 64};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
-                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) {
-    set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
-    return DHSA_ECUDA;
-  }
-  return DHSA_OK;
 }
 
 template <int D, int STAGES>
 static int launch(const CUtensorMap& mk, const CUtensorMap& mv, const void* q, int64_t cache_rows,
                   int items, int ipu, int GH, const int32_t* tiles, int64_t cap,
                   const int32_t* nt, int splits, void* out, void* ws, int32_t* cnt,
-                  cudaStream_t s) {
+                  int32_t* ready, cudaStream_t s) {
   constexpr int STAGE_BYTES = 2 * (D / 64) * 64 * 128;
   const size_t smem = (size_t)STAGES * STAGE_BYTES + 1024;
   cudaError_t e = cudaFuncSetAttribute(attn_mma_kernel<D, STAGES>,
@@ -269,17 +245,31 @@ static int launch(const CUtensorMap& mk, const CUtensorMap& mv, const void* q, i
     return DHSA_ECUDA;
   }
   const float scale_log2 = (float)(1.4426950408889634 / sqrt((double)D));
-  dim3 grid((unsigned)splits, (unsigned)items);
-  attn_mma_kernel<D, STAGES><<<grid, 160, smem, s>>>(
-      mk, mv, (const __nv_bfloat16*)q, cache_rows, ipu, GH, tiles, cap, nt, splits,
-      (__nv_bfloat16*)out, ws, cnt, scale_log2);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)splits, (unsigned)items);
+  cfg.blockDim = dim3(160);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = ready ? 1 : 0;  // early launch only when per-item flags gate the work
+  e = cudaLaunchKernelEx(&cfg, attn_mma_kernel<D, STAGES>, mk, mv, (const __nv_bfloat16*)q,
+                         cache_rows, ipu, GH, tiles, cap, nt, splits, (__nv_bfloat16*)out, ws,
+                         cnt, scale_log2, ready);
+  if (e != cudaSuccess) {
+    set_error("dhsa_attn(bf16): %s", cudaGetErrorString(e));
+    return DHSA_ECUDA;
+  }
   return check_launch("dhsa_attn(bf16)");
 }
 
 int attn_mma_bf16(const void* q, const void* k_cache, const void* v_cache,
                   int64_t cache_unit_stride, int64_t cache_rows, int items, int items_per_unit,
                   int GH, int D, const int32_t* tiles, int64_t tile_cap, const int32_t* ntiles,
-                  int splits, void* out, void* ws, int32_t* counters, cudaStream_t s) {
+                  int splits, void* out, void* ws, int32_t* counters, int32_t* ready,
+                  cudaStream_t s) {
   DHSA_REQUIRE(D == 64 || D == 128, "dhsa_attn(bf16): D must be 64 or 128, got %d", D);
   DHSA_REQUIRE(cache_unit_stride == cache_rows * D,
                "dhsa_attn(bf16): cache units must be dense [rows][D]");
@@ -290,15 +280,15 @@ int attn_mma_bf16(const void* q, const void* k_cache, const void* v_cache,
   const int64_t rows = (int64_t)units * cache_rows;
   DHSA_REQUIRE(rows < (1ll << 31), "dhsa_attn(bf16): cache too large for 32-bit TMA rows");
   CUtensorMap mk, mv;
-  int rc = make_map(&mk, k_cache, rows, D);
+  int rc = make_tmap_2d(&mk, k_cache, rows, D, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16);
   if (rc) return rc;
-  rc = make_map(&mv, v_cache, rows, D);
+  rc = make_tmap_2d(&mv, v_cache, rows, D, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16);
   if (rc) return rc;
   if (D == 128)
     return launch<128, 3>(mk, mv, q, cache_rows, items, items_per_unit, GH, tiles, tile_cap,
-                          ntiles, splits, out, ws, counters, s);
+                          ntiles, splits, out, ws, counters, ready, s);
   return launch<64, 6>(mk, mv, q, cache_rows, items, items_per_unit, GH, tiles, tile_cap, ntiles,
-                       splits, out, ws, counters, s);
+                       splits, out, ws, counters, ready, s);
 }
 
 }  // namespace dhsa

@@ -27,6 +27,11 @@ inline int check_launch(const char* what) {
     }                                \
   } while (0)
 
+// 2-D TMA view [rows][D] of a 16-bit tensor (bf16 / fp16): 64 x 64-element
+// boxes (64 rows x 128 B) with 128-byte swizzle (tmap.cu).
+int make_tmap_2d(CUtensorMap* map, const void* base, int64_t rows, int D,
+                 CUtensorMapDataType dtype);
+
 inline bool valid_layout(const dhsa_layout& l) {
   if (!l.plen) return false;
   if (l.bounds) return l.nchunks != nullptr;

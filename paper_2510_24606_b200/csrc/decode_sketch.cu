@@ -41,10 +41,6 @@
 
 namespace dhsa {
 
-constexpr int kConsumerWarps = 8;
-constexpr int kScoreThreads = (kConsumerWarps + 1) * 32;
-constexpr int kSliceBytes = 16384;
-constexpr int kStages = 4;
 constexpr int kSelectThreads = 512;
 constexpr int kSmallUncertain = 1024;
 
@@ -79,6 +75,7 @@ struct SketchArgs {
   int smem_select;
   int n_max;
   int advance;
+  int32_t* ready;           // [items] select -> attention flags (zero at rest) or null
   unsigned long long* dbg;  // optional per-CTA phase timestamps (DHSA_DEBUG_TIMING)
 };
 
@@ -124,130 +121,171 @@ __device__ __forceinline__ int tr_index(int k, int glane) {
 }
 
 // ------------------------------------------------------------ score stream --
+// Tensor-core sketch scores: S^T[chunk][head] = C''[chunk][:] . q'[head][:]
+// with mma.sync m16n8k16 (fp16 in, fp32 accumulate).  A = 16 sketch rows from
+// a 128B-swizzled TMA tile (ldmatrix, conflict free), B = the G query heads of
+// the kv group (N = 8 columns, heads >= G zero) held in registers for the
+// whole unit, each head scaled by a power of two 2^-kq so bf16 q is exact in
+// fp16.  4 consumer warps x 16 rows per 64-chunk slice; one producer thread
+// keeps kStages slices in flight with 2-D TMA loads.
+constexpr int kTcConsumers = 4;
+constexpr int kTcThreads = (kTcConsumers + 1) * 32;
+constexpr int kTcStages = 4;
+constexpr int kSliceRows = 64;
+
 template <int D, int G, int AGG>
-__global__ __launch_bounds__(kScoreThreads) void sketch_score_kernel(SketchArgs a) {
-  constexpr int LG = D / 8;                  // lanes per chunk row (8 halfs = 16 B each)
-  constexpr int CPL = 32 / LG;               // chunk rows per warp load
-  constexpr int SLICE = kSliceBytes / (D * 2);  // chunks per slice (64 or 128)
-  constexpr int CPW = SLICE / kConsumerWarps;   // chunks per warp per slice (8 or 16)
-  constexpr int LOADS = CPW / CPL;           // 4
-  constexpr int NV = LOADS * G;
-  constexpr int NF = NV >= LG ? NV / LG : 1;
-  constexpr int REP = NV >= LG ? 1 : LG / NV;
-  extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages];
-  __shared__ float hv[kConsumerWarps][CPW][G];
+__global__ __launch_bounds__(kTcThreads) void sketch_score_kernel(
+    const __grid_constant__ CUtensorMap tmS, SketchArgs a) {
+  constexpr int NB = D / 64;       // 128-byte column boxes per row
+  constexpr int BOX = 64 * 128;    // 64 rows x 128 B
+  constexpr int TILE = NB * BOX;
+  constexpr int STAGE = TILE;
+  constexpr int KS = D / 16;
+  static_assert(G <= 8, "N = 8 columns");
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full_bar[kTcStages], empty_bar[kTcStages];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t s_begin = a.total_slices * blockIdx.x / gridDim.x;
-  const int64_t s_end = a.total_slices * (blockIdx.x + 1) / gridDim.x;
+  const int rows_per_unit = (int)(a.sk_stride / D);
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < kTcStages; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], kConsumerWarps);
+      mbar_init(&empty_bar[s], kTcConsumers);
     }
     fence_barrier_init();
   }
   __syncthreads();
+  pdl_trigger();  // the select kernel may launch (and run its prologue) right away
+  // contiguous slice range per CTA; (unit, first chunk) advanced incrementally
+  const int spu = a.slices_per_unit;
+  const int64_t s_begin = a.total_slices * blockIdx.x / gridDim.x;
+  const int64_t s_end = a.total_slices * (blockIdx.x + 1) / gridDim.x;
+  int u = (int)(s_begin / spu);
+  int c0 = (int)(s_begin - (int64_t)u * spu) * kSliceRows;
+  int nc = a.lay.num_chunks(u);
 
-  if (warp == kConsumerWarps) {
-    // ---------------- producer: one thread drives the TMA bulk ring ----------------
+  if (warp == kTcConsumers) {
     if (lane == 0) {
+      prefetch_tmap(&tmS);
       int it = 0;
       for (int64_t sl = s_begin; sl < s_end; ++sl) {
-        const int u = (int)(sl / a.slices_per_unit);
-        const int c0 = (int)(sl % a.slices_per_unit) * SLICE;
-        const int nch = min(SLICE, a.lay.num_chunks(u) - c0);
-        if (nch <= 0) continue;
-        const int st = it % kStages;
-        if (it >= kStages) mbar_wait(&empty_bar[st], ((it / kStages) + 1) & 1);
-        const uint32_t bytes = (uint32_t)nch * D * 2;
-        mbar_expect_tx(&full_bar[st], bytes);
-        bulk_load(smem + st * kSliceBytes, a.sketch + (int64_t)u * a.sk_stride + (int64_t)c0 * D,
-                  bytes, &full_bar[st]);
-        ++it;
+        if (c0 < nc) {
+          const int st = it % kTcStages;
+          if (it >= kTcStages) mbar_wait(&empty_bar[st], ((it / kTcStages) + 1) & 1);
+          mbar_expect_tx(&full_bar[st], TILE);
+          const int row = u * rows_per_unit + c0;
+#pragma unroll
+          for (int b = 0; b < NB; ++b) tma_load_2d(smem + st * STAGE + b * BOX, &tmS, &full_bar[st], b * 64, row);
+          ++it;
+        }
+        c0 += kSliceRows;
+        if (c0 >= spu * kSliceRows) {
+          c0 = 0;
+          ++u;
+          if (sl + 1 < s_end) nc = a.lay.num_chunks(u);
+        }
       }
     }
     return;
   }
 
   // ---------------- consumers ----------------
-  const int sub = lane / LG, gl = lane % LG, dl = gl * 8;
-  float qf[G][8];
+  const int hcol = lane >> 2;  // B column (head) owned for the fragment
+  uint32_t qb[KS][2];
+  int kq0 = 0, kq1 = 0;        // scale exponents of the two heads in this lane's C columns
   int cur_u = -1;
+  const int mi = lane >> 3, r8 = lane & 7;
+  const int arow = warp * 16 + (mi & 1) * 8 + r8;  // A row addressed by this lane
   int it = 0;
-  for (int64_t sl = s_begin; sl < s_end; ++sl) {
-    const int u = (int)(sl / a.slices_per_unit);
-    const int c0 = (int)(sl % a.slices_per_unit) * SLICE;
-    const int nch = min(SLICE, a.lay.num_chunks(u) - c0);
-    if (nch <= 0) continue;
+  for (int64_t sl = s_begin; sl < s_end; ++sl, c0 += kSliceRows) {
+    if (c0 >= spu * kSliceRows) {
+      c0 = 0;
+      ++u;
+      nc = a.lay.num_chunks(u);
+    }
+    if (c0 >= nc) continue;
     if (u != cur_u) {
       cur_u = u;
+      // B fragments of q'^T: head hcol, dims 16ks + 2(lane&3) + {0,1} (+8)
+      float qv[KS][4];
+      float amax = 0.f;
+      const __nv_bfloat16* qrow = a.q + (int64_t)(u * G + (hcol < G ? hcol : 0)) * D;
 #pragma unroll
-      for (int h = 0; h < G; ++h) {
-        const uint4 raw = *reinterpret_cast<const uint4*>(a.q + (int64_t)(u * G + h) * D + dl);
-        const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+      for (int ks = 0; ks < KS; ++ks) {
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 f = __bfloat1622float2(p2[e]);
-          qf[h][2 * e] = f.x;
-          qf[h][2 * e + 1] = f.y;
+        for (int e = 0; e < 2; ++e) {
+          const int d = 16 * ks + 2 * (lane & 3) + 8 * e;
+          float2 f = make_float2(0.f, 0.f);
+          if (hcol < G) f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(qrow + d));
+          qv[ks][2 * e] = f.x;
+          qv[ks][2 * e + 1] = f.y;
+          amax = fmaxf(amax, fmaxf(fabsf(f.x), fabsf(f.y)));
         }
       }
-    }
-    const int st = it % kStages;
-    mbar_wait(&full_bar[st], (it / kStages) & 1);
-    const unsigned char* buf = smem + st * kSliceBytes;
-    float part[NV];
+      amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
+      amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 2));
+      const int kq = amax > 0.f ? ilogbf(amax) + 1 - 14 : 0;  // max|q| 2^-kq < 2^14
 #pragma unroll
-    for (int i = 0; i < LOADS; ++i) {
-      const int cl = warp * CPW + i * CPL + sub;  // chunk within the slice
-      uint4 raw = make_uint4(0, 0, 0, 0);
-      if (cl < nch) raw = *reinterpret_cast<const uint4*>(buf + cl * (D * 2) + dl * 2);
-      const __half2* p2 = reinterpret_cast<const __half2*>(&raw);
-      float cv[8];
+      for (int ks = 0; ks < KS; ++ks) {
+        const __half2 lo = __floats2half2_rn(ldexpf(qv[ks][0], -kq), ldexpf(qv[ks][1], -kq));
+        const __half2 hi = __floats2half2_rn(ldexpf(qv[ks][2], -kq), ldexpf(qv[ks][3], -kq));
+        qb[ks][0] = *reinterpret_cast<const uint32_t*>(&lo);
+        qb[ks][1] = *reinterpret_cast<const uint32_t*>(&hi);
+      }
+      // C columns of this lane are heads 2(lane&3), 2(lane&3)+1: fetch their exponents
+      kq0 = __shfl_sync(0xffffffffu, kq, 4 * (2 * (lane & 3)));
+      kq1 = __shfl_sync(0xffffffffu, kq, 4 * (2 * (lane & 3) + 1));
+    }
+    const int st = it % kTcStages;
+    mbar_wait(&full_bar[st], (it / kTcStages) & 1);
+    const uint32_t base = smem_u32(smem + st * STAGE);
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int kch = 2 * ks + (mi >> 1);
+      const uint32_t addr = base + (kch >> 3) * BOX + arow * 128 + (((kch & 7) ^ (arow & 7)) << 4);
+      uint32_t a0, a1, a2, a3;
+      ldsm_x4(addr, a0, a1, a2, a3);
+      mma_f16(acc, a0, a1, a2, a3, qb[ks][0], qb[ks][1]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[st]);
+    ++it;
+    // acc[0..1]: row warp*16 + lane/4, heads 2(lane&3)+{0,1}; acc[2..3]: row + 8
+    const int h0 = 2 * (lane & 3);
+    float v[4];
+    v[0] = h0 < G ? ldexpf(acc[0], kq0) : -INFINITY;
+    v[1] = h0 + 1 < G ? ldexpf(acc[1], kq1) : -INFINITY;
+    v[2] = h0 < G ? ldexpf(acc[2], kq0) : -INFINITY;
+    v[3] = h0 + 1 < G ? ldexpf(acc[3], kq1) : -INFINITY;
+    const int r0 = warp * 16 + (lane >> 2);
+    if constexpr (AGG == DHSA_AGG_NONE) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const float2 f = __half22float2(p2[e]);
-        cv[2 * e] = f.x;
-        cv[2 * e + 1] = f.y;
+        const int h = h0 + (e & 1), r = r0 + 8 * (e >> 1);
+        if (h < G && c0 + r < nc) a.approx[(int64_t)(u * G + h) * a.sc_stride + c0 + r] = v[e];
       }
+    } else {
+      float x = (AGG == DHSA_AGG_MAX) ? fmaxf(v[0], v[1]) : (h0 < G ? v[0] : 0.f) + (h0 + 1 < G ? v[1] : 0.f);
+      float y = (AGG == DHSA_AGG_MAX) ? fmaxf(v[2], v[3]) : (h0 < G ? v[2] : 0.f) + (h0 + 1 < G ? v[3] : 0.f);
 #pragma unroll
-      for (int h = 0; h < G; ++h) {
-        float s = 0.f;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) s = fmaf(qf[h][e], cv[e], s);
-        part[i * G + h] = s;
+      for (int o = 1; o <= 2; o <<= 1) {
+        const float xo = __shfl_xor_sync(0xffffffffu, x, o);
+        const float yo = __shfl_xor_sync(0xffffffffu, y, o);
+        x = (AGG == DHSA_AGG_MAX) ? fmaxf(x, xo) : x + xo;
+        y = (AGG == DHSA_AGG_MAX) ? fmaxf(y, yo) : y + yo;
       }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty_bar[st]);  // smem slice consumed
-    ++it;
-    transpose_reduce_f<NV, LG>(part, lane);
-    if (gl % REP == 0) {
-#pragma unroll
-      for (int k = 0; k < NF; ++k) {
-        const int idx = tr_index<NV, LG>(k, gl);
-        const int i = idx / G, h = idx % G;
-        hv[warp][i * CPL + sub][h] = part[k];
-      }
-    }
-    __syncwarp();
-    if (lane < CPW) {
-      const int c = c0 + warp * CPW + lane;
-      if (warp * CPW + lane < nch) {
-        if constexpr (AGG == DHSA_AGG_NONE) {
-#pragma unroll
-          for (int h = 0; h < G; ++h) a.approx[(int64_t)(u * G + h) * a.sc_stride + c] = hv[warp][lane][h];
-        } else {
-          float s = hv[warp][lane][0];
-#pragma unroll
-          for (int h = 1; h < G; ++h) s = (AGG == DHSA_AGG_MAX) ? fmaxf(s, hv[warp][lane][h]) : s + hv[warp][lane][h];
-          a.approx[(int64_t)u * a.sc_stride + c] = (AGG == DHSA_AGG_MEAN) ? s / (float)G : s;
+      if ((lane & 3) == 0) {
+        if (AGG == DHSA_AGG_MEAN) {
+          x = x / (float)G;
+          y = y / (float)G;
         }
+        if (c0 + r0 < nc) a.approx[(int64_t)u * a.sc_stride + c0 + r0] = x;
+        if (c0 + r0 + 8 < nc) a.approx[(int64_t)u * a.sc_stride + c0 + r0 + 8] = y;
       }
     }
-    __syncwarp();
   }
 }
 
@@ -298,6 +336,7 @@ __global__ __launch_bounds__(kSelectThreads) void sketch_select_kernel(SketchArg
   uint32_t* ak = reinterpret_cast<uint32_t*>(lens + a.n_max);
   int32_t* unc = reinterpret_cast<int32_t*>(ak + a.n_max);
 
+  pdl_trigger();  // the attention kernel may launch once every select CTA is resident
   DBG_T(0);
   // ---- prologue: every global load of the step issued before one barrier ----
   for (int i = tid; i < G * D; i += kSelectThreads)
@@ -355,6 +394,8 @@ __global__ __launch_bounds__(kSelectThreads) void sketch_select_kernel(SketchArg
       }
     }
   }
+  // the approximate scores are complete once the score grid has finished
+  pdl_wait();
   __syncthreads();
   DBG_T(1);
 
@@ -366,9 +407,10 @@ __global__ __launch_bounds__(kSelectThreads) void sketch_select_kernel(SketchArg
   const float kexp = a.sinfo[4 * u + 0];
   const double scale = ldexp(1.0, -(int)kexp);  // sketch units per score unit
   const double cmax = a.sinfo[4 * u + 1], dmax = a.sinfo[4 * u + 2];
-  // fp32 summation of D exact products + the G-term head mean (<= 8 more adds)
-  constexpr double gam = (double)(D + 8) * 5.9604644775390625e-08 /
-                         (1.0 - (double)(D + 8) * 5.9604644775390625e-08);
+  // accumulation: mma.sync fp32 accumulation of D exact fp16 products (bounded
+  // conservatively by 2^-14 sum|p|, ~4x the published truncating-alignment
+  // model of 8 x 17 x 2^-23) + the head mean + q fp16 subnormal rounding
+  constexpr double gam = 6.103515625e-05 + 1e-6;
 
   const int nitems = AGG == DHSA_AGG_NONE ? G : 1;
   for (int it = 0; it < nitems; ++it) {
@@ -506,7 +548,14 @@ __global__ __launch_bounds__(kSelectThreads) void sketch_select_kernel(SketchArg
                                           a.tile_tokens, a.tiles + (int64_t)s * a.tile_cap * 2,
                                           a.tile_cap, a.ntiles + s, sh);
   }
-  if (tid == 0 && a.advance) a.gen_count[u] = g + 1;  // masks.py:236
+  __syncthreads();
+  if (tid == 0) {
+    if (a.advance) a.gen_count[u] = g + 1;  // masks.py:236
+    if (a.ready) {  // tiles, running sum and appended k/v are published together
+      __threadfence();
+      for (int it = 0; it < nitems; ++it) st_release(a.ready + (AGG == DHSA_AGG_NONE ? u * G + it : u), 1);
+    }
+  }
   DBG_T(8);
 }
 
@@ -571,21 +620,24 @@ __global__ __launch_bounds__(256) void sketch_build_kernel(const double* __restr
 template <int D, int G, int AGG>
 static int launch_step(const SketchArgs& a, int U, size_t sel_smem, cudaStream_t s) {
   auto score = sketch_score_kernel<D, G, AGG>;
-  static_assert(kStages * kSliceBytes <= 200 * 1024, "ring too large");
-  const int ring = kStages * kSliceBytes;
+  constexpr int ring = kTcStages * (D / 64) * 64 * 128 + 1024;
   cudaError_t e = cudaFuncSetAttribute(score, cudaFuncAttributeMaxDynamicSharedMemorySize, ring);
   if (e != cudaSuccess) {
     set_error("dhsa_decode_step_bf16: %s", cudaGetErrorString(e));
     return DHSA_ECUDA;
   }
+  CUtensorMap tm;
+  int rc = make_tmap_2d(&tm, a.sketch, (int64_t)U * (a.sk_stride / D), D,
+                        CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+  if (rc) return rc;
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, score, kScoreThreads, ring);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, score, kTcThreads, ring);
   int64_t grid = (int64_t)sms * (per_sm < 1 ? 1 : per_sm);
   if (grid > a.total_slices) grid = a.total_slices;
-  score<<<(unsigned)grid, kScoreThreads, ring, s>>>(a);
-  int rc = check_launch("dhsa_decode_step_bf16(score)");
+  score<<<(unsigned)grid, kTcThreads, ring, s>>>(tm, a);
+  rc = check_launch("dhsa_decode_step_bf16(score)");
   if (rc) return rc;
   auto sel = sketch_select_kernel<D, G, AGG>;
   if (sel_smem > 48 * 1024) {
@@ -595,7 +647,21 @@ static int launch_step(const SketchArgs& a, int U, size_t sel_smem, cudaStream_t
       return DHSA_ECUDA;
     }
   }
-  sel<<<U, kSelectThreads, sel_smem, s>>>(a);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)U);
+  cfg.blockDim = dim3(kSelectThreads);
+  cfg.dynamicSmemBytes = sel_smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, sel, a);
+  if (e != cudaSuccess) {
+    set_error("dhsa_decode_step_bf16(select): %s", cudaGetErrorString(e));
+    return DHSA_ECUDA;
+  }
   return check_launch("dhsa_decode_step_bf16(select)");
 }
 
@@ -656,7 +722,7 @@ extern "C" int dhsa_decode_step_bf16(
     const void* k_new, const void* v_new, void* k_cache, void* v_cache, int64_t cache_unit_stride,
     dhsa_layout layout, int U, int G, int D, int agg, int64_t budget, int tile_tokens,
     int32_t* tiles, int64_t tile_cap, int32_t* ntiles, float* approx, int64_t sc_stride,
-    void* scratch, int advance, dhsa_stream_t stream) {
+    void* scratch, int32_t* ready, int advance, dhsa_stream_t stream) {
   DHSA_REQUIRE(q && sketch && sinfo && centroids && gen_sum && gen_count && tiles && ntiles &&
                    approx,
                "dhsa_decode_step_bf16: null pointer");
@@ -686,8 +752,7 @@ extern "C" int dhsa_decode_step_bf16(
   a.lay = Layout(layout);
   a.approx = approx;
   a.sc_stride = sc_stride;
-  const int slice = kSliceBytes / (D * 2);
-  a.slices_per_unit = (layout.max_chunks + slice - 1) / slice;
+  a.slices_per_unit = (layout.max_chunks + kSliceRows - 1) / kSliceRows;
   a.total_slices = (int64_t)a.slices_per_unit * U;
   a.budget = budget;
   a.tile_tokens = tile_tokens;
@@ -696,6 +761,7 @@ extern "C" int dhsa_decode_step_bf16(
   a.ntiles = ntiles;
   a.n_max = layout.max_chunks + 1;
   a.advance = advance;
+  a.ready = ready;
   if (const char* e = getenv("DHSA_DEBUG_TIMING")) a.dbg = (unsigned long long*)strtoull(e, nullptr, 0);
   const int64_t need = dhsa_sketch_select_scratch_size(layout.max_chunks);
   size_t smem = 0;

@@ -108,6 +108,7 @@ class SparseDecoder:
                                       **kw)
             self.sinfo = torch.zeros(self.U, 4, dtype=torch.float32, **kw)
             self.approx = torch.empty(self.items, self.nc_cap + 1, dtype=torch.float32, **kw)
+            self.ready = torch.zeros(self.items, dtype=torch.int32, **kw)
             per_unit = _lib.load().dhsa_sketch_select_scratch_size(self.nc_cap)
             self.scratch = (torch.empty(self.U * per_unit, dtype=torch.uint8, **kw)
                             if per_unit > 0 else None)
@@ -171,7 +172,8 @@ class SparseDecoder:
                           _lib.ptr(self.v_cache), self.L_cap * self.D, lay, self.U, self.G,
                           self.D, agg, self.budget, self.tile, _lib.ptr(self.tiles),
                           self.tile_cap, _lib.ptr(self.ntiles), _lib.ptr(self.approx),
-                          self.nc_cap + 1, _lib.ptr(self.scratch), 1, st)
+                          self.nc_cap + 1, _lib.ptr(self.scratch), _lib.ptr(self.ready), 1,
+                          st)
             return [("score_select", fused), attn]
 
         def score():
@@ -197,7 +199,8 @@ class SparseDecoder:
                   _lib.ptr(self.v_cache), self.L_cap * self.D, self.L_cap, self.items,
                   self.G if self.per_head else 1, self.GH, self.D, _lib.ptr(self.tiles),
                   self.tile_cap, _lib.ptr(self.ntiles), self.splits, _lib.ptr(out),
-                  _lib.ptr(self.ws), _lib.ptr(self.counters), st)
+                  _lib.ptr(self.ws), _lib.ptr(self.counters),
+                  _lib.ptr(self.ready) if self.scoring == "sketch" else 0, st)
 
     @property
     def kernels_per_step(self) -> int:
