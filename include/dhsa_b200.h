@@ -196,6 +196,80 @@ int dhsa_decode_step_bf16(const void* q, const void* sketch, int64_t sk_unit_str
                           int64_t sc_stride, void* scratch, int32_t* ready, int advance,
                           dhsa_stream_t stream);
 
+/* ---- sequence-sharded split-KV decode (1M-token contexts over GPUs) --------
+ * A sequence is cut into W contiguous shards (one per GPU); shard r holds
+ * prompt chunks [chunk_offset, chunk_offset + nchunks) with their K/V,
+ * centroids and sketch; the tail shard (owns_tail) also holds the generated
+ * chunk and receives the newest token.  One step:
+ *   1. dhsa_decode_candidates_bf16 on every shard: local certified walk with
+ *      the GLOBAL budget -> candidate records (exact fp64 score, global chunk
+ *      id, length, local start) of every chunk with a positive local take;
+ *   2. all-gather of the fixed-size candidate rows (NCCL);
+ *   3. dhsa_split_select: the global walk over all shards' candidates
+ *      (identical on every shard) -> this shard's tiles (+ self on the tail);
+ *   4. dhsa_attn_partials: attention over the local tiles -> unnormalised
+ *      (m, l, acc) records per q row;
+ *   5. all-gather of the records (NCCL) and dhsa_merge_partials.
+ * The union of local candidate sets contains every chunk of the global
+ * selection (a chunk with fewer than R tokens ranked above it globally has
+ * fewer than R above it locally), so the result equals the unsharded walk. */
+typedef struct {
+  double score;   /* exact fp64 aggregated score (q . c_j, masks.py:165) */
+  int32_t gid;    /* global chunk id (prompt chunks in order, then the generated chunk) */
+  int32_t len;    /* chunk length in tokens */
+  int32_t lo;     /* first token of the chunk in the shard's cache */
+  int32_t pad;
+} dhsa_split_cand;  /* one candidate; row = [count (int32, -1 = overflow) | pad][cap records] */
+
+typedef struct {
+  int32_t chunk_offset;  /* global id of this shard's chunk 0 */
+  int32_t total_chunks;  /* global prompt chunk count (= generated chunk id) */
+  int32_t total_prompt;  /* global prompt length; the newest token is row total_prompt + g */
+  int32_t owns_tail;     /* 1 on the shard holding the generated chunk and the newest token */
+} dhsa_split_shard;
+
+/* Step 1 (bf16 sketch path; arguments as dhsa_decode_step_bf16).  gen_count
+ * is the GLOBAL generated count on every shard (not advanced here); k_new /
+ * v_new / caches are used on the tail shard only (NULL elsewhere).
+ * cand: [items][cand_stride bytes], cand_stride >= 24 * (cand_cap + 1). */
+int dhsa_decode_candidates_bf16(const void* q, const void* sketch, int64_t sk_unit_stride,
+                                const float* sinfo, const double* centroids,
+                                int64_t c_unit_stride, double* gen_sum, const int32_t* gen_count,
+                                const void* k_new, const void* v_new, void* k_cache,
+                                void* v_cache, int64_t cache_unit_stride, dhsa_layout layout,
+                                int U, int G, int D, int agg, int64_t budget,
+                                dhsa_split_shard shard, void* cand, int64_t cand_stride,
+                                int cand_cap, float* approx, int64_t sc_stride, void* scratch,
+                                dhsa_stream_t stream);
+
+/* Step 3: the global walk (masks.topk_row order: score desc, chunk asc) over
+ * the W gathered candidate rows of every item (gathered + r * rank_stride
+ * bytes = shard r's [items][cand_stride] block) with R = min(budget, row+1)-1,
+ * row = total_prompt + gen_count[u].  Emits tiles for this shard's chunks
+ * (candidates of shard `rank`) and, on the tail shard, the self tile at local
+ * row self_row[u] = local prompt length + gen_count[u].  advance: gen_count
+ * += 1 afterwards (every shard keeps the global count). */
+int dhsa_split_select(const void* gathered, int W, int64_t rank_stride, int64_t cand_stride,
+                      int cand_cap, int items, int items_per_unit, int32_t* gen_count,
+                      const int32_t* plen, int total_prompt, int64_t budget, int rank,
+                      int owns_tail, int tile_tokens, int32_t* tiles, int64_t tile_cap,
+                      int32_t* ntiles, int advance, dhsa_stream_t stream);
+
+/* Step 4: dhsa_attn (bf16) writing, per q row, the unnormalised record
+ * [m (log2 domain), l, acc[D]] (fp32) instead of the output; an empty
+ * selection gives m = -inf, l = 0, acc = 0. */
+int dhsa_attn_partials(const void* q, const void* k_cache, const void* v_cache,
+                       int64_t cache_unit_stride, int64_t cache_rows, int items,
+                       int items_per_unit, int GH, int D, const int32_t* tiles,
+                       int64_t tile_cap, const int32_t* ntiles, int splits, float* records,
+                       void* workspace, int32_t* counters, dhsa_stream_t stream);
+
+/* Step 5: o = sum_r acc_r 2^(m_r - m*) / sum_r l_r 2^(m_r - m*), m* = max_r m_r,
+ * over W record blocks (records + r * rank_stride floats, [rows][D+2] each);
+ * out [rows][D] in dtype (BF16 / F32). */
+int dhsa_merge_partials(const float* records, int W, int64_t rank_stride, int rows, int D,
+                        int dtype, void* out, dhsa_stream_t stream);
+
 /* f_upsample (masks.upsample, masks.py:87-100): out[i][j] = s[chunk(i)][chunk(j)]
  * for an n x n chunk-score matrix and bounds [n+1]; out is L x L fp64.  Only
  * the drop-in API uses it — the selection kernels never materialise it. */

@@ -33,6 +33,12 @@ class Layout(C.Structure):
     ]
 
 
+class ShardSpec(C.Structure):
+    """dhsa_split_shard"""
+    _fields_ = [("chunk_offset", C.c_int32), ("total_chunks", C.c_int32),
+                ("total_prompt", C.c_int32), ("owns_tail", C.c_int32)]
+
+
 _SIGS = {
     "dhsa_last_error": (C.c_char_p, []),
     "dhsa_version": (C.c_int, []),
@@ -58,6 +64,16 @@ _SIGS = {
                                         vp, vp, C.c_int64, Layout, C.c_int, C.c_int, C.c_int,
                                         C.c_int, C.c_int64, C.c_int, vp, C.c_int64, vp, vp,
                                         C.c_int64, vp, vp, C.c_int, vp]),
+    "dhsa_decode_candidates_bf16": (C.c_int, [vp, vp, C.c_int64, vp, vp, C.c_int64, vp, vp, vp,
+                                              vp, vp, vp, C.c_int64, Layout, C.c_int, C.c_int,
+                                              C.c_int, C.c_int, C.c_int64, ShardSpec, vp,
+                                              C.c_int64, C.c_int, vp, C.c_int64, vp, vp]),
+    "dhsa_split_select": (C.c_int, [vp, C.c_int, C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int,
+                                    vp, vp, C.c_int, C.c_int64, C.c_int, C.c_int, C.c_int, vp,
+                                    C.c_int64, vp, C.c_int, vp]),
+    "dhsa_attn_partials": (C.c_int, [vp, vp, vp, C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int,
+                                     C.c_int, vp, C.c_int64, vp, C.c_int, vp, vp, vp, vp]),
+    "dhsa_merge_partials": (C.c_int, [vp, C.c_int, C.c_int64, C.c_int, C.c_int, C.c_int, vp, vp]),
 }
 
 _lib = None

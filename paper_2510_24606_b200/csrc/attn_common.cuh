@@ -38,10 +38,13 @@ __device__ __forceinline__ bool split_arrive(int32_t* counters, int item, int sp
   return s_last != 0;
 }
 
-// Merge the `splits` partial records of `item` and write out[q_row][d].
+// Merge the `splits` partial records of `item` and write out[q_row][d], or,
+// when `rec_out` is given, one merged (m, l, acc) record per q row (the
+// sequence-sharded split-KV path merges those across GPUs, splitkv.cu).
 // The m of every record is in log2 units (scores * log2(e) / sqrt(D)).
 template <typename T, typename A>
-__device__ void merge_partials(const void* ws, int item, int splits, int GH, int D, T* out) {
+__device__ void merge_partials(const void* ws, int item, int splits, int GH, int D, T* out,
+                               A* rec_out = nullptr) {
   for (int hd = threadIdx.x; hd < GH * D; hd += blockDim.x) {
     const int h = hd / D, d = hd - h * D;
     A mstar = -INFINITY;
@@ -58,7 +61,16 @@ __device__ void merge_partials(const void* ws, int item, int splits, int GH, int
       l += w * ld_cg(p + 1);
       acc += w * ld_cg(p + 2 + d);
     }
-    out[((int64_t)item * GH + h) * D + d] = from_acc<T>(acc / l);
+    if (rec_out) {
+      A* r = rec_out + ((int64_t)item * GH + h) * (D + 2);
+      if (d == 0) {
+        r[0] = mstar;
+        r[1] = l;
+      }
+      r[2 + d] = acc;
+    } else {
+      out[((int64_t)item * GH + h) * D + d] = from_acc<T>(acc / l);
+    }
   }
 }
 

@@ -18,7 +18,7 @@ int attn_mma_bf16(const void* q, const void* k_cache, const void* v_cache,
                   int64_t cache_unit_stride, int64_t cache_rows, int items, int items_per_unit,
                   int GH, int D, const int32_t* tiles, int64_t tile_cap, const int32_t* ntiles,
                   int splits, void* out, void* ws, int32_t* counters, int32_t* ready,
-                  cudaStream_t s);
+                  float* rec_out, cudaStream_t s);
 
 constexpr int kGHMax = 8;
 
@@ -193,8 +193,26 @@ extern "C" int dhsa_attn(int dtype, const void* q, const void* k_cache, const vo
     case DHSA_BF16:
       return attn_mma_bf16(q, k_cache, v_cache, cache_unit_stride, cache_rows, items,
                            items_per_unit, GH, D, tiles, tile_cap, ntiles, splits, out, workspace,
-                           counters, ready, s);
+                           counters, ready, nullptr, s);
   }
   set_error("dhsa_attn: unknown dtype %d", dtype);
   return DHSA_EINVAL;
+}
+
+extern "C" int dhsa_attn_partials(const void* q, const void* k_cache, const void* v_cache,
+                                  int64_t cache_unit_stride, int64_t cache_rows, int items,
+                                  int items_per_unit, int GH, int D, const int32_t* tiles,
+                                  int64_t tile_cap, const int32_t* ntiles, int splits,
+                                  float* records, void* workspace, int32_t* counters,
+                                  dhsa_stream_t stream) {
+  DHSA_REQUIRE(q && k_cache && v_cache && tiles && ntiles && records,
+               "dhsa_attn_partials: null pointer");
+  DHSA_REQUIRE(items >= 1 && items_per_unit >= 1 && GH >= 1 && GH <= kGHMax && splits >= 1 &&
+                   tile_cap >= 1,
+               "dhsa_attn_partials: bad shape (GH <= 8)");
+  DHSA_REQUIRE(splits == 1 || (workspace && counters),
+               "dhsa_attn_partials: split-KV needs workspace");
+  return attn_mma_bf16(q, k_cache, v_cache, cache_unit_stride, cache_rows, items, items_per_unit,
+                       GH, D, tiles, tile_cap, ntiles, splits, nullptr, workspace, counters,
+                       nullptr, records, (cudaStream_t)stream);
 }

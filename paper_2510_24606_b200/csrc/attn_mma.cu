@@ -29,7 +29,7 @@ __global__ __launch_bounds__(160) void attn_mma_kernel(
     const __nv_bfloat16* __restrict__ q, int64_t cache_rows, int items_per_unit, int GH,
     const int32_t* __restrict__ tiles, int64_t tile_cap, const int32_t* __restrict__ ntiles,
     int splits, __nv_bfloat16* __restrict__ out, void* ws, int32_t* counters, float scale_log2,
-    int32_t* ready) {
+    int32_t* ready, float* __restrict__ rec_out) {
   constexpr int NB = D / 64;                  // 128-byte column boxes per row
   constexpr int BOX = 64 * 128;               // one box: 64 token rows x 128 B
   constexpr int STAGE_BYTES = 2 * NB * BOX;   // K + V
@@ -210,7 +210,14 @@ __global__ __launch_bounds__(160) void attn_mma_kernel(
       lsum += wgt * r[1];
       a += wgt * r[2 + d];
     }
-    if (direct) {
+    if (direct && rec_out) {  // unnormalised record for a cross-GPU merge
+      float* r = rec_out + ((int64_t)item * GH + h) * (D + 2);
+      if (d == 0) {
+        r[0] = mstar;
+        r[1] = lsum;
+      }
+      r[2 + d] = a;
+    } else if (direct) {
       out[((int64_t)item * GH + h) * D + d] = __float2bfloat16_rn(a / lsum);
     } else {
       float* p = partial_ptr<float>(ws, item, split, splits, h, GH, D);
@@ -226,7 +233,7 @@ __global__ __launch_bounds__(160) void attn_mma_kernel(
     return;
   }
   if (split_arrive(counters, item, splits)) {
-    merge_partials<__nv_bfloat16, float>(ws, item, splits, GH, D, out);
+    merge_partials<__nv_bfloat16, float>(ws, item, splits, GH, D, out, rec_out);
     if (ready && threadIdx.x == 0) ready[item] = 0;  // every sibling CTA is past its wait
   }
 }
@@ -235,7 +242,7 @@ template <int D, int STAGES>
 static int launch(const CUtensorMap& mk, const CUtensorMap& mv, const void* q, int64_t cache_rows,
                   int items, int ipu, int GH, const int32_t* tiles, int64_t cap,
                   const int32_t* nt, int splits, void* out, void* ws, int32_t* cnt,
-                  int32_t* ready, cudaStream_t s) {
+                  int32_t* ready, float* rec_out, cudaStream_t s) {
   constexpr int STAGE_BYTES = 2 * (D / 64) * 64 * 128;
   const size_t smem = (size_t)STAGES * STAGE_BYTES + 1024;
   cudaError_t e = cudaFuncSetAttribute(attn_mma_kernel<D, STAGES>,
@@ -257,7 +264,7 @@ static int launch(const CUtensorMap& mk, const CUtensorMap& mv, const void* q, i
   cfg.numAttrs = ready ? 1 : 0;  // early launch only when per-item flags gate the work
   e = cudaLaunchKernelEx(&cfg, attn_mma_kernel<D, STAGES>, mk, mv, (const __nv_bfloat16*)q,
                          cache_rows, ipu, GH, tiles, cap, nt, splits, (__nv_bfloat16*)out, ws,
-                         cnt, scale_log2, ready);
+                         cnt, scale_log2, ready, rec_out);
   if (e != cudaSuccess) {
     set_error("dhsa_attn(bf16): %s", cudaGetErrorString(e));
     return DHSA_ECUDA;
@@ -269,7 +276,7 @@ int attn_mma_bf16(const void* q, const void* k_cache, const void* v_cache,
                   int64_t cache_unit_stride, int64_t cache_rows, int items, int items_per_unit,
                   int GH, int D, const int32_t* tiles, int64_t tile_cap, const int32_t* ntiles,
                   int splits, void* out, void* ws, int32_t* counters, int32_t* ready,
-                  cudaStream_t s) {
+                  float* rec_out, cudaStream_t s) {
   DHSA_REQUIRE(D == 64 || D == 128, "dhsa_attn(bf16): D must be 64 or 128, got %d", D);
   DHSA_REQUIRE(cache_unit_stride == cache_rows * D,
                "dhsa_attn(bf16): cache units must be dense [rows][D]");
@@ -286,9 +293,9 @@ int attn_mma_bf16(const void* q, const void* k_cache, const void* v_cache,
   if (rc) return rc;
   if (D == 128)
     return launch<128, 3>(mk, mv, q, cache_rows, items, items_per_unit, GH, tiles, tile_cap,
-                          ntiles, splits, out, ws, counters, ready, s);
+                          ntiles, splits, out, ws, counters, ready, rec_out, s);
   return launch<64, 6>(mk, mv, q, cache_rows, items, items_per_unit, GH, tiles, tile_cap, ntiles,
-                       splits, out, ws, counters, ready, s);
+                       splits, out, ws, counters, ready, rec_out, s);
 }
 
 }  // namespace dhsa

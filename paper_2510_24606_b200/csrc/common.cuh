@@ -10,6 +10,9 @@
 
 namespace dhsa {
 
+using SplitCand = dhsa_split_cand;
+static_assert(sizeof(SplitCand) == 24, "candidate record is 24 bytes");
+
 // ----------------------------------------------------------------- dtypes --
 
 template <typename T> struct Acc { using type = float; };

@@ -77,6 +77,16 @@ struct SketchArgs {
   int advance;
   int32_t* ready;           // [items] select -> attention flags (zero at rest) or null
   unsigned long long* dbg;  // optional per-CTA phase timestamps (DHSA_DEBUG_TIMING)
+  // sequence-sharded split-KV mode (dhsa_decode_candidates_bf16): this shard
+  // holds global prompt chunks [chunk_offset, chunk_offset + nchunks); the
+  // tail shard also holds the generated chunk (global id total_chunks) and
+  // the newest token.  Instead of tiles, every chunk the local exact walk
+  // gives a positive take is written as a candidate record.
+  int split;
+  int32_t chunk_offset, total_chunks, total_prompt, owns_tail;
+  unsigned char* cand;      // [items][cand_stride] bytes: header + SplitCand[cand_cap]
+  int64_t cand_stride;
+  int cand_cap;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -318,6 +328,63 @@ __device__ __forceinline__ double agg_d(const double* v, int nh) {
   return s;
 }
 
+// Split-KV: every chunk with a positive local take (takes in lens[]) becomes a
+// candidate record with its exact fp64 score (the same arithmetic as the
+// re-scoring above), global chunk id, full length and local start token.
+// The global walk (splitkv.cu) over the candidates of all shards then equals
+// the unsharded walk: a chunk with a positive global take has fewer than R
+// tokens ranked above it globally, hence locally, so it is a local candidate.
+template <int D, int G, int AGG>
+__device__ void emit_candidates(const SketchArgs& a, const UnitChunks& uc, const int32_t* takes,
+                                int32_t* list, int n, int s, const double (*qd)[D], int h0, int nh,
+                                double gex, int u) {
+  constexpr int NW = kSelectThreads / 32;
+  __shared__ int s_ncand;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_ncand = 0;
+  __syncthreads();
+  for (int c = tid; c < n; c += kSelectThreads)
+    if (takes[c] > 0) list[atomicAdd(&s_ncand, 1)] = c;
+  __syncthreads();
+  const int nc = s_ncand;
+  unsigned char* row = a.cand + (int64_t)s * a.cand_stride;
+  SplitCand* rec = reinterpret_cast<SplitCand*>(row) + 1;
+  for (int i = warp; i < nc && i < a.cand_cap; i += NW) {
+    const int c = list[i];
+    int lo, len;
+    uc.chunk(c, lo, len);
+    double ex;
+    if (c < uc.nc) {
+      const double* crow = a.cent + (int64_t)u * a.c_stride + (int64_t)c * D;
+      double part[G];
+#pragma unroll
+      for (int h = 0; h < G; ++h) part[h] = 0.0;
+#pragma unroll
+      for (int d = lane; d < D; d += 32) {
+        const double cv = crow[d];
+#pragma unroll
+        for (int h = 0; h < G; ++h) part[h] = fma(qd[h][d], cv, part[h]);
+      }
+#pragma unroll
+      for (int h = 0; h < G; ++h) part[h] = warp_sum(part[h]);
+      ex = agg_d<G, AGG>(part + h0, nh);
+    } else {
+      ex = gex;
+    }
+    if (lane == 0) {
+      SplitCand r;
+      r.score = ex;
+      r.gid = c < uc.nc ? a.chunk_offset + c : a.total_chunks;
+      r.len = len;
+      r.lo = lo;
+      r.pad = 0;
+      rec[i] = r;
+    }
+  }
+  if (tid == 0) reinterpret_cast<int32_t*>(row)[0] = nc <= a.cand_cap ? nc : -1;
+  __syncthreads();
+}
+
 template <int D, int G, int AGG>
 __global__ __launch_bounds__(kSelectThreads) void sketch_select_kernel(SketchArgs a) {
   constexpr int NW = kSelectThreads / 32;
@@ -342,6 +409,7 @@ __global__ __launch_bounds__(kSelectThreads) void sketch_select_kernel(SketchArg
   for (int i = tid; i < G * D; i += kSelectThreads)
     qd[i / D][i % D] = to_f64(a.q[(int64_t)u * G * D + i]);
   const int g = a.gen_count[u];
+  const int gl = (a.split && !a.owns_tail) ? 0 : g;  // generated tokens held by this shard
   constexpr int DV = D / 32;
   if (warp < G) {
     double t = 0.0;
@@ -369,8 +437,8 @@ __global__ __launch_bounds__(kSelectThreads) void sketch_select_kernel(SketchArg
     double part[G];
 #pragma unroll
     for (int h = 0; h < G; ++h) part[h] = 0.0;
-    if (g >= 1) {
-      const double rs = __dsqrt_rn((double)g);
+    if (gl >= 1) {
+      const double rs = __dsqrt_rn((double)gl);
 #pragma unroll
       for (int v = 0; v < DV; ++v) {
         const double cg = __ddiv_rn(gv[v], rs);
@@ -384,7 +452,7 @@ __global__ __launch_bounds__(kSelectThreads) void sketch_select_kernel(SketchArg
 #pragma unroll
       for (int h = 0; h < G; ++h) s_gen[h] = part[h];
     if (a.k_new) {  // masks.py:235: after the read above; k/v appended at row P+g
-      const int64_t pos = (int64_t)(a.lay.prompt_len(u) + g) * D;
+      const int64_t pos = (int64_t)(a.lay.prompt_len(u) + gl) * D;
 #pragma unroll
       for (int v = 0; v < DV; ++v) {
         const int d = lane + 32 * v;
@@ -399,9 +467,10 @@ __global__ __launch_bounds__(kSelectThreads) void sketch_select_kernel(SketchArg
   __syncthreads();
   DBG_T(1);
 
-  UnitChunks uc{a.lay, u, a.lay.num_chunks(u), g, a.lay.prompt_len(u)};
-  const int n = uc.nc + (g >= 1 ? 1 : 0);
-  const int row = uc.P + g;
+  UnitChunks uc{a.lay, u, a.lay.num_chunks(u), gl, a.lay.prompt_len(u)};
+  const int n = uc.nc + (gl >= 1 ? 1 : 0);
+  const int wloc = uc.P + gl;  // tokens the walk ranges over (self excluded)
+  const int row = a.split ? a.total_prompt + g : uc.P + g;  // global row of the newest token
   const int64_t keep = a.budget < (int64_t)row + 1 ? a.budget : (int64_t)row + 1;
   const uint32_t R = (uint32_t)(keep - 1);
   const float kexp = a.sinfo[4 * u + 0];
@@ -453,7 +522,7 @@ __global__ __launch_bounds__(kSelectThreads) void sketch_select_kernel(SketchArg
     uint64_t prefix = 0, mask = 0;
     uint32_t rrem = R;
     bool done = false;
-    if (R > 0 && R < (uint32_t)row) {
+    if (R > 0 && R < (uint32_t)wloc) {
       uint32_t p32, m32, r32;
       DBG_T(2);
       radix_threshold<kSelectThreads, uint32_t>(ak, lens, n, R, sh, p32, m32, r32);
@@ -534,19 +603,24 @@ __global__ __launch_bounds__(kSelectThreads) void sketch_select_kernel(SketchArg
         for (int i = tid; i < nu; i += kSelectThreads) lens[unc[i]] = take[i];
         __syncthreads();
         DBG_T(6);
-        emit_takes<kSelectThreads>(uc, lens, n, row, a.tile_tokens,
-                                   a.tiles + (int64_t)s * a.tile_cap * 2, a.tile_cap,
-                                   a.ntiles + s, sh);
+        if (!a.split)
+          emit_takes<kSelectThreads>(uc, lens, n, row, a.tile_tokens,
+                                     a.tiles + (int64_t)s * a.tile_cap * 2, a.tile_cap,
+                                     a.ntiles + s, sh);
         DBG_T(7);
         done = true;
       } else {
         radix_threshold<kSelectThreads, uint64_t>(key64, lens, n, R, sh, prefix, mask, rrem);
       }
     }
-    if (!done)
+    if (!done && a.split)
+      walk_takes<kSelectThreads, uint64_t>(key64, lens, n, R, prefix, mask, rrem, sh);
+    else if (!done)
       walk_emit<kSelectThreads, uint64_t>(uc, key64, lens, n, R, prefix, mask, rrem, row,
                                           a.tile_tokens, a.tiles + (int64_t)s * a.tile_cap * 2,
                                           a.tile_cap, a.ntiles + s, sh);
+    if (a.split)
+      emit_candidates<D, G, AGG>(a, uc, lens, unc, n, s, qd, h0, nh, gex, u);
   }
   __syncthreads();
   if (tid == 0) {
@@ -716,15 +790,17 @@ extern "C" int dhsa_sketch_build(const double* centroids, int64_t c_unit_stride,
   return check_launch("dhsa_sketch_build");
 }
 
-extern "C" int dhsa_decode_step_bf16(
+static int decode_step_impl(
     const void* q, const void* sketch, int64_t sk_unit_stride, const float* sinfo,
     const double* centroids, int64_t c_unit_stride, double* gen_sum, int32_t* gen_count,
     const void* k_new, const void* v_new, void* k_cache, void* v_cache, int64_t cache_unit_stride,
     dhsa_layout layout, int U, int G, int D, int agg, int64_t budget, int tile_tokens,
     int32_t* tiles, int64_t tile_cap, int32_t* ntiles, float* approx, int64_t sc_stride,
-    void* scratch, int32_t* ready, int advance, dhsa_stream_t stream) {
-  DHSA_REQUIRE(q && sketch && sinfo && centroids && gen_sum && gen_count && tiles && ntiles &&
-                   approx,
+    void* scratch, int32_t* ready, int advance, dhsa_stream_t stream,
+    const dhsa_split_shard* shard = nullptr, void* cand = nullptr, int64_t cand_stride = 0,
+    int cand_cap = 0) {
+  DHSA_REQUIRE(q && sketch && sinfo && centroids && gen_sum && gen_count &&
+                   (shard || (tiles && ntiles)) && approx,
                "dhsa_decode_step_bf16: null pointer");
   DHSA_REQUIRE(budget >= 1, "budget must be >= 1");
   DHSA_REQUIRE(D == 64 || D == 128, "dhsa_decode_step_bf16: D must be 64 or 128");
@@ -762,6 +838,24 @@ extern "C" int dhsa_decode_step_bf16(
   a.n_max = layout.max_chunks + 1;
   a.advance = advance;
   a.ready = ready;
+  if (shard) {
+    DHSA_REQUIRE(cand && cand_cap >= 1 && cand_stride >= (int64_t)sizeof(SplitCand) * (cand_cap + 1) &&
+                     cand_stride % 8 == 0,
+                 "dhsa_decode_candidates_bf16: bad candidate buffer");
+    DHSA_REQUIRE(shard->chunk_offset >= 0 && shard->total_chunks >= shard->chunk_offset &&
+                     shard->total_prompt >= 1,
+                 "dhsa_decode_candidates_bf16: bad shard description");
+    a.split = 1;
+    a.chunk_offset = shard->chunk_offset;
+    a.total_chunks = shard->total_chunks;
+    a.total_prompt = shard->total_prompt;
+    a.owns_tail = shard->owns_tail;
+    a.cand = (unsigned char*)cand;
+    a.cand_stride = cand_stride;
+    a.cand_cap = cand_cap;
+    a.advance = 0;
+    a.ready = nullptr;
+  }
   if (const char* e = getenv("DHSA_DEBUG_TIMING")) a.dbg = (unsigned long long*)strtoull(e, nullptr, 0);
   const int64_t need = dhsa_sketch_select_scratch_size(layout.max_chunks);
   size_t smem = 0;
@@ -778,4 +872,31 @@ extern "C" int dhsa_decode_step_bf16(
   cudaStream_t s = (cudaStream_t)stream;
   if (D == 128) return dispatch_agg<128>(agg, G, a, U, smem, s);
   return dispatch_agg<64>(agg, G, a, U, smem, s);
+}
+
+extern "C" int dhsa_decode_step_bf16(
+    const void* q, const void* sketch, int64_t sk_unit_stride, const float* sinfo,
+    const double* centroids, int64_t c_unit_stride, double* gen_sum, int32_t* gen_count,
+    const void* k_new, const void* v_new, void* k_cache, void* v_cache, int64_t cache_unit_stride,
+    dhsa_layout layout, int U, int G, int D, int agg, int64_t budget, int tile_tokens,
+    int32_t* tiles, int64_t tile_cap, int32_t* ntiles, float* approx, int64_t sc_stride,
+    void* scratch, int32_t* ready, int advance, dhsa_stream_t stream) {
+  return decode_step_impl(q, sketch, sk_unit_stride, sinfo, centroids, c_unit_stride, gen_sum,
+                          gen_count, k_new, v_new, k_cache, v_cache, cache_unit_stride, layout, U,
+                          G, D, agg, budget, tile_tokens, tiles, tile_cap, ntiles, approx,
+                          sc_stride, scratch, ready, advance, stream);
+}
+
+extern "C" int dhsa_decode_candidates_bf16(
+    const void* q, const void* sketch, int64_t sk_unit_stride, const float* sinfo,
+    const double* centroids, int64_t c_unit_stride, double* gen_sum, const int32_t* gen_count,
+    const void* k_new, const void* v_new, void* k_cache, void* v_cache, int64_t cache_unit_stride,
+    dhsa_layout layout, int U, int G, int D, int agg, int64_t budget, dhsa_split_shard shard,
+    void* cand, int64_t cand_stride, int cand_cap, float* approx, int64_t sc_stride,
+    void* scratch, dhsa_stream_t stream) {
+  return decode_step_impl(q, sketch, sk_unit_stride, sinfo, centroids, c_unit_stride, gen_sum,
+                          const_cast<int32_t*>(gen_count), k_new, v_new, k_cache, v_cache,
+                          cache_unit_stride, layout, U, G, D, agg, budget, 64, nullptr, 2, nullptr,
+                          approx, sc_stride, scratch, nullptr, 0, stream, &shard, cand,
+                          cand_stride, cand_cap);
 }

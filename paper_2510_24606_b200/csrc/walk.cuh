@@ -194,12 +194,11 @@ __device__ void emit_takes(const View& view, const int32_t* takes, int n, int ro
   __syncthreads();
 }
 
-// Turn (prefix, mask, rrem) into per-chunk takes (written back into lens[])
-// and emit the tiles.  R == 0 emits self only.
-template <int NT, typename K, class View>
-__device__ void walk_emit(const View& view, const K* keys, int32_t* lens, int n, uint32_t R,
-                          K prefix, K mask, uint32_t rrem, int row, int tile_tokens,
-                          int32_t* out, int64_t cap, int32_t* ntiles_out, WalkShared& sh) {
+// Turn (prefix, mask, rrem) into per-chunk takes, written back into lens[].
+// R == 0 takes nothing.
+template <int NT, typename K>
+__device__ void walk_takes(const K* keys, int32_t* lens, int n, uint32_t R, K prefix, K mask,
+                           uint32_t rrem, WalkShared& sh) {
   const int tid = threadIdx.x;
   const int cpt = (n + NT - 1) / NT;
   const int c0 = min(tid * cpt, n), c1 = min(c0 + cpt, n);
@@ -228,6 +227,14 @@ __device__ void walk_emit(const View& view, const K* keys, int32_t* lens, int n,
     }
   }
   __syncthreads();
+}
+
+// walk_takes, then emit the tiles.  R == 0 emits self only.
+template <int NT, typename K, class View>
+__device__ void walk_emit(const View& view, const K* keys, int32_t* lens, int n, uint32_t R,
+                          K prefix, K mask, uint32_t rrem, int row, int tile_tokens,
+                          int32_t* out, int64_t cap, int32_t* ntiles_out, WalkShared& sh) {
+  walk_takes<NT, K>(keys, lens, n, R, prefix, mask, rrem, sh);
   emit_takes<NT>(view, lens, n, row, tile_tokens, out, cap, ntiles_out, sh);
 }
 
