@@ -470,6 +470,90 @@ def run_gpu_c4(args):
         dist.destroy_process_group()
 
 
+def run_gpu_c5(args):
+    """C5: sparse prefill of one 32K-token sequence (Llama-3-8B attention
+    shape, bf16), tcgen05 tiles over the selected blocks, top-k sweep.
+    Reports the whole prefill time per K and the attention kernel's tensor
+    throughput against the measured bf16 peak (algorithmic flops =
+    4 * sum_i min(i+1, budget) * D * Hq)."""
+    import torch
+
+    from paper_2510_24606_b200.prefill import SparsePrefill
+
+    world, rank, local = dist_setup()
+    B, Hq, Hkv, D, L = 1, 32, 8, 128, 32768
+    W, S = args.warmup, args.steps
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(77 + rank)
+    q = torch.randn(B, Hq, L, D, device="cuda", generator=gen).bfloat16()
+    k = torch.randn(B, Hkv, L, D, device="cuda", generator=gen).bfloat16()
+    v = torch.randn(B, Hkv, L, D, device="cuda", generator=gen).bfloat16()
+    out = torch.empty_like(q)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > L2 (126 MB)
+    tf_peak = tf_sust = None
+    pp = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(pp):
+        with open(pp) as f:
+            d = json.load(f)
+        tf_peak, tf_sust = d.get("bf16_tflops"), d.get("bf16_tflops_sustained")
+    peak = tf_peak or 1590.0
+    sweep = []
+    with ClockSampler(local) as clk:
+        for K in args.c5_topk:
+            pf = SparsePrefill(B, Hq, Hkv, D, L, top_k=K, agg="max")
+            stg = pf.stages(q, k, v, out)
+            for _ in range(W):
+                for _, fn in stg:
+                    fn()
+            torch.cuda.synchronize()
+            pf.check_capacity()
+            names = [n for n, _ in stg]
+            acc = {n: 0.0 for n in names}
+            tot = 0.0
+            for _ in range(S):
+                flush.zero_()  # L2 flushed before every timed prefill
+                ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(stg) + 1)]
+                ev[0].record()
+                for i, (_, fn) in enumerate(stg):
+                    fn()
+                    ev[i + 1].record()
+                torch.cuda.synchronize()
+                for i, n in enumerate(names):
+                    acc[n] += ev[i].elapsed_time(ev[i + 1])
+                tot += ev[0].elapsed_time(ev[-1])
+            ms = max_over_ranks(tot / S, world)
+            attn_ms = acc["attn"] / S
+            fl = pf.flops()
+            sweep.append({"top_k": K, "budget": pf.budget, "ms": ms,
+                          "breakdown_ms": {n: acc[n] / S for n in names},
+                          "tflops_algorithmic": fl / 1e12,
+                          "attn_tflops": fl / (attn_ms * 1e-3) / 1e12,
+                          "attn_frac_of_peak": fl / (attn_ms * 1e-3) / 1e12 / peak,
+                          "prefill_tokens_per_s": B * L / (ms * 1e-3)})
+    head = next((x for x in sweep if x["top_k"] == 64), sweep[0])
+    result = {
+        "metric": "sparse prefill ms per 32K-token sequence (C5); tensor TFLOP/s vs roofline",
+        "value": head["ms"], "unit": "ms", "n_gpus": world, "steps": S, "warmup": W,
+        "ms_per_step": head["ms"], "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic N(0,1) q/k/v",
+        "config": {"workload": f"C5 sparse prefill: B={B}, Hq={Hq}, Hkv={Hkv}, d={D}, L={L}, "
+                               "block=64, group-shared max selection, tcgen05 tiles",
+                   "l2": "flushed (256 MB write) before every timed prefill",
+                   "headline_top_k": head["top_k"]},
+        "roofline": {"bound": "tensor", "kernel": "attn", "achieved": head["attn_tflops"],
+                     "peak": peak, "unit": "TFLOP/s", "frac": head["attn_frac_of_peak"],
+                     "peak_source": "measured (MEASURED_PEAKS.json bf16_tflops)" if tf_peak
+                     else "fallback (B200_PROFILING.md)", "peak_sustained": tf_sust},
+        "sweep": sweep, "gpu_launches": 5 * S, "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -503,7 +587,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="C3", choices=sorted(CONFIGS) + ["C5"])
+    ap.add_argument("--c5-topk", type=int, nargs="+", default=[16, 32, 64, 128, 256])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--breakdown-steps", type=int, default=6)
     ap.add_argument("--e2e-steps", type=int, default=10)
@@ -521,6 +606,8 @@ def main():
         run_reference(args)
     elif args.config == "C4":
         run_gpu_c4(args)
+    elif args.config == "C5":
+        run_gpu_c5(args)
     else:
         run_gpu(args)
 

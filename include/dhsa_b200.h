@@ -270,6 +270,44 @@ int dhsa_attn_partials(const void* q, const void* k_cache, const void* v_cache,
 int dhsa_merge_partials(const float* records, int W, int64_t rank_stride, int rows, int D,
                         int dtype, void* out, dhsa_stream_t stream);
 
+/* ---- sparse prefill on tcgen05 (config C5) ---------------------------------
+ * prefill_mask (masks.py:143-150) + dense_attention(seq, mask) (core.py:98-119)
+ * for B sequences, q [U*G][L][D], k/v [U][L][D] bf16 (U = B * kv heads, G q
+ * heads per kv head), static 64-token chunks, D = 128.  The L x L upsampled
+ * matrix is never built.
+ *
+ * dhsa_prefill_scores: S[s][l][c] (c <= l) = agg_j Qc[q(s,j)][l] . Kc[u(s)][c]
+ * in fp64 (chunk_repr.py:97-103; harness.py:288-306 max / mean over the G
+ * q-heads of unit s, or agg NONE: one row per q head, s = u*G + j).
+ * q_centroids [U*G][n_chunks][D], k_centroids [U][n_chunks][D] from
+ * dhsa_centroids; scores [S][n_chunks][n_chunks]. */
+int dhsa_prefill_scores(const double* q_centroids, const double* k_centroids, int U, int G,
+                        int n_chunks, int D, int agg, double* scores, dhsa_stream_t stream);
+
+/* Plan entries per (selection row, query chunk) needed for `budget`. */
+int dhsa_prefill_plan_capacity(int64_t budget, int block);
+
+/* Per (s, query chunk l): the chunks of the walk (masks.topk_row order: score
+ * desc, chunk asc) that some row of chunk l takes tokens from, as int32x4
+ * {start, len, W, flags} in walk order (W = tokens of non-diagonal chunks
+ * ranked before; flags bit0 = the diagonal chunk ranks before, bit1 = this is
+ * the diagonal chunk, always last).  Row i of chunk l takes
+ * clamp(R_i - W - (bit0 ? i - b_l : 0), 0, len) lowest tokens of an entry
+ * (the diagonal: clamp(R_i - W, 0, i - b_l)) plus self, R_i =
+ * min(budget, i+1) - 1 — exactly topk_row on the upsampled row.
+ * plans [S][n_chunks][cap] int32x4, nplan [S][n_chunks] (-1 = overflow). */
+int dhsa_prefill_plan(const double* scores, int S, int n_chunks, int L, int block,
+                      int64_t budget, int cap, void* plans, int32_t* nplan,
+                      dhsa_stream_t stream);
+
+/* Block-sparse attention of every query row over its planned tokens:
+ * softmax(K[idx] q / sqrt(D)) @ V[idx] (core.py:113-118) with tcgen05.mma
+ * (bf16 operands from TMA-staged 128B-swizzled shared memory, fp32 TMEM
+ * accumulators), one CTA per (plan, <= 4 q heads).  out [U*G][L][D] bf16. */
+int dhsa_prefill_attn(const void* q, const void* k, const void* v, int U, int G, int L, int D,
+                      int block, int agg, int64_t budget, const void* plans,
+                      const int32_t* nplan, int cap, void* out, dhsa_stream_t stream);
+
 /* f_upsample (masks.upsample, masks.py:87-100): out[i][j] = s[chunk(i)][chunk(j)]
  * for an n x n chunk-score matrix and bounds [n+1]; out is L x L fp64.  Only
  * the drop-in API uses it — the selection kernels never materialise it. */

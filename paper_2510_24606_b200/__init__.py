@@ -24,7 +24,7 @@ __all__ = [
     "ChunkReps", "aggregate_chunk", "aggregate_rows", "build_chunk_reps", "chunk_similarity",
     "CostCounters", "SparsityMask", "upsample", "topk_row", "mask_from_chunk_scores",
     "prefill_mask", "decode_mask_row", "DecodeSession",
-    "SparseDecoder",
+    "SparseDecoder", "SparsePrefill", "SplitKVShard", "SplitKVGroup",
 ]
 
 
@@ -33,4 +33,12 @@ def __getattr__(name):
         from .decode import SparseDecoder
 
         return SparseDecoder
+    if name == "SparsePrefill":
+        from .prefill import SparsePrefill
+
+        return SparsePrefill
+    if name in ("SplitKVShard", "SplitKVGroup"):
+        from . import splitkv
+
+        return getattr(splitkv, name)
     raise AttributeError(name)

@@ -74,6 +74,13 @@ _SIGS = {
     "dhsa_attn_partials": (C.c_int, [vp, vp, vp, C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int,
                                      C.c_int, vp, C.c_int64, vp, C.c_int, vp, vp, vp, vp]),
     "dhsa_merge_partials": (C.c_int, [vp, C.c_int, C.c_int64, C.c_int, C.c_int, C.c_int, vp, vp]),
+    "dhsa_prefill_scores": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp,
+                                      vp]),
+    "dhsa_prefill_plan_capacity": (C.c_int, [C.c_int64, C.c_int]),
+    "dhsa_prefill_plan": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int,
+                                    vp, vp, vp]),
+    "dhsa_prefill_attn": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                    C.c_int, C.c_int64, vp, vp, C.c_int, vp, vp]),
 }
 
 _lib = None

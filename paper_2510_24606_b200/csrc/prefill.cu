@@ -1,0 +1,523 @@
+// Sparse prefill (config C5): chunk scores, per-query-chunk selection plans and
+// block-sparse attention on the tcgen05 tensor cores (TMEM accumulators,
+// TMA-staged 128B-swizzled operand tiles).
+//
+// Reference path: prefill_mask (masks.py:143-150) = build_chunk_reps
+// (chunk_repr.py:85-94, centroids of Q and K) -> chunk_similarity
+// (chunk_repr.py:97-103, S_c = Q_c K_c^T, no scaling) -> [optional head
+// aggregation, harness.py:288-306] -> mask_from_chunk_scores (masks.py:125-140:
+// upsample + topk_row per row), then dense_attention(seq, mask)
+// (core.py:98-119).  The L x L upsampled matrix is never built:
+//
+//  K7  prefill_scores_kernel  S[s][l][c] (c <= l) in fp64, aggregated over
+//                             the q-heads sharing a selection row;
+//  K8  prefill_plan_kernel    one CTA per (selection row s, query chunk l):
+//                             every row of chunk l walks the SAME chunk order
+//                             (score desc, chunk asc); only the diagonal
+//                             chunk's effective length d_i = i - b_l and the
+//                             token budget R_i = min(budget, i+1) - 1 differ
+//                             per row.  The plan lists, in walk order, every
+//                             non-diagonal chunk some row of the chunk takes
+//                             tokens from (weighted radix select with the
+//                             largest R of the chunk) with W = tokens of
+//                             non-diagonal chunks ranked before it and a flag
+//                             "diagonal ranks before", plus the diagonal.  Row
+//                             i then takes clamp(R_i - W - [diag before]*d_i,
+//                             0, len) lowest tokens of each entry (SURVEY.md
+//                             Appendix A) and self;
+//  K9  prefill_attn_kernel    one CTA per (plan, <= 4 q-heads): a 128- or
+//                             256-row query tile (64 rows per head, one M=128
+//                             tcgen05 tile per 2 heads), S = Q K^T and O += P V
+//                             per selected 64-token KV block with tcgen05.mma
+//                             (fp32 accumulators in TMEM), per-row masks from
+//                             the plan, online softmax with one thread per
+//                             query row (tcgen05.ld 32x32b), P through
+//                             swizzled shared memory.
+#include "capi.cuh"
+#include "tc05.cuh"
+#include "walk.cuh"
+
+namespace dhsa {
+
+// ------------------------------------------------------------------- K7 --
+// S[s][l][c] = agg_{j in heads(s)} Qc[q(s,j)][l] . Kc[u(s)][c] for c <= l, fp64
+// (dot products accumulated in dimension order, aggregated max / mean).
+__global__ __launch_bounds__(256) void prefill_scores_kernel(
+    const double* __restrict__ qc, const double* __restrict__ kc, int nc, int D, int G,
+    int per_head, int agg, double* __restrict__ out) {
+  __shared__ double a[16][33];
+  __shared__ double b[16][33];
+  const int s = blockIdx.z;
+  const int i0 = blockIdx.y * 16, j0 = blockIdx.x * 16;
+  if (j0 > i0 + 15) return;  // strictly above the diagonal: never read
+  const int ty = threadIdx.x / 16, tx = threadIdx.x % 16;
+  const int u = per_head ? s / G : s;
+  const int nh = per_head ? 1 : G;
+  const int h0 = per_head ? s : s * G;
+  const double* K = kc + (int64_t)u * nc * D;
+  double res = 0.0;
+  for (int j = 0; j < nh; ++j) {
+    const double* Q = qc + (int64_t)(h0 + j) * nc * D;
+    double acc = 0.0;
+    for (int d0 = 0; d0 < D; d0 += 32) {
+      for (int e = threadIdx.x; e < 16 * 32; e += 256) {
+        const int r = e / 32, c = e % 32;
+        a[r][c] = (i0 + r < nc && d0 + c < D) ? Q[(int64_t)(i0 + r) * D + d0 + c] : 0.0;
+        b[r][c] = (j0 + r < nc && d0 + c < D) ? K[(int64_t)(j0 + r) * D + d0 + c] : 0.0;
+      }
+      __syncthreads();
+#pragma unroll 8
+      for (int c = 0; c < 32; ++c) acc = fma(a[ty][c], b[tx][c], acc);
+      __syncthreads();
+    }
+    if (j == 0) res = acc;
+    else if (agg == DHSA_AGG_MAX) res = fmax(res, acc);
+    else res = res + acc;
+  }
+  if (agg == DHSA_AGG_MEAN && nh > 1) res = res / (double)nh;
+  if (i0 + ty < nc && j0 + tx < nc) out[((int64_t)s * nc + i0 + ty) * nc + j0 + tx] = res;
+}
+
+// ------------------------------------------------------------------- K8 --
+constexpr int kPlanThreads = 128;
+
+__global__ __launch_bounds__(kPlanThreads) void prefill_plan_kernel(
+    const double* __restrict__ S, int nc, int L, int block, int64_t budget, int cap,
+    int4* __restrict__ plans, int32_t* __restrict__ nplan) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ WalkShared sh;
+  __shared__ int s_n;
+  uint64_t* key = reinterpret_cast<uint64_t*>(smem_raw);
+  int32_t* lens = reinterpret_cast<int32_t*>(key + nc);
+  int32_t* list = lens + nc;
+  const int l = blockIdx.x, s = blockIdx.y, tid = threadIdx.x;
+  const double* srow = S + ((int64_t)s * nc + l) * nc;
+  const int bl = l * block, el = min(bl + block, L);
+  // the largest token budget among the rows of chunk l (its last row)
+  const int64_t rmax64 = (budget < (int64_t)el ? budget : (int64_t)el) - 1;
+  const uint32_t Rmax = (uint32_t)rmax64;
+  for (int c = tid; c < l; c += kPlanThreads) {
+    key[c] = order_key(srow[c]);
+    lens[c] = block;  // chunks before the diagonal are full
+  }
+  const uint64_t kdiag = order_key(srow[l]);
+  if (tid == 0) s_n = 0;
+  __syncthreads();
+  // takes of the walk over the non-diagonal chunks with budget Rmax
+  if (l > 0) {
+    if (Rmax >= (uint32_t)bl) {
+      // every earlier chunk is kept whole by the last row
+    } else if (Rmax == 0) {
+      for (int c = tid; c < l; c += kPlanThreads) lens[c] = 0;
+      __syncthreads();
+    } else {
+      uint64_t prefix, mask;
+      uint32_t rrem;
+      radix_threshold<kPlanThreads, uint64_t>(key, lens, l, Rmax, sh, prefix, mask, rrem);
+      walk_takes<kPlanThreads, uint64_t>(key, lens, l, Rmax, prefix, mask, rrem, sh);
+    }
+    for (int c = tid; c < l; c += kPlanThreads)
+      if (lens[c] > 0) list[atomicAdd(&s_n, 1)] = c;
+  }
+  __syncthreads();
+  const int n = s_n;
+  int4* out = plans + ((int64_t)s * nc + l) * cap;
+  // rank = position in the walk order; W = full chunk tokens ranked before
+  int wdiag_local = 0;
+  for (int i = tid; i < n; i += kPlanThreads) {
+    const int c = list[i];
+    const uint64_t kc = key[c];
+    int rank = 0;
+    for (int j = 0; j < n; ++j) {
+      const int cj = list[j];
+      const uint64_t kj = key[cj];
+      rank += (kj > kc || (kj == kc && cj < c)) ? 1 : 0;
+    }
+    // every selected chunk is full (block tokens); W = rank * block
+    const int diag_before = kdiag > kc ? 1 : 0;  // tie: the lower index (c < l) first
+    if (rank < cap - 1) out[rank] = make_int4(c * block, block, rank * block, diag_before);
+    if (!diag_before) wdiag_local += block;
+  }
+  wdiag_local = warp_sum(wdiag_local);
+  __shared__ int s_wd;
+  if (tid == 0) s_wd = 0;
+  __syncthreads();
+  if ((tid & 31) == 0 && wdiag_local) atomicAdd(&s_wd, wdiag_local);
+  __syncthreads();
+  if (tid == 0) {
+    if (n + 1 > cap) {
+      nplan[s * nc + l] = -1;  // capacity error (reported by the host)
+    } else {
+      out[n] = make_int4(bl, el - bl, s_wd, 2);  // the diagonal chunk (self always)
+      nplan[s * nc + l] = n + 1;
+    }
+  }
+}
+
+// ------------------------------------------------------------------- K9 --
+struct PrefillArgs {
+  const int4* plans;
+  const int32_t* nplan;
+  int cap, nc, L, block;
+  int64_t budget;
+  int G, per_head, heads_per_cta, slices;
+  __nv_bfloat16* out;  // [q heads][L][D]
+  float scale_log2;
+};
+
+template <int MT, int NST>
+struct PrefillSmem {
+  static constexpr int Q = MT * 2 * 16384;         // [mt][D half][128 rows][128 B]
+  static constexpr int KV = 2 * 2 * 8192;           // K [half][64][128B] + V [half][64][128B]
+  static constexpr int P = MT * 16384;             // one P buffer: [mt][128 rows][128 B]
+  static constexpr int q_off = 0;
+  static constexpr int kv_off = Q;
+  static constexpr int p_off = Q + NST * KV;
+  static constexpr int total = p_off + 2 * P + 1024;  // + alignment slack
+};
+
+template <int MT, int NST>
+__global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_kernel(
+    const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+    const __grid_constant__ CUtensorMap tmV, PrefillArgs a) {
+  using SM = PrefillSmem<MT, NST>;
+  constexpr int D = 128;
+  constexpr uint32_t kTmemCols = MT * 256;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t kv_full[NST], kv_empty[NST], s_full[2], p_full[2], o_done,
+      q_full;
+  __shared__ uint32_t s_tmem;
+  __shared__ int4 s_plan[288];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int hs = blockIdx.x;                   // head slice of the selection row
+  const int l = a.nc - 1 - blockIdx.y;         // heavy (late) query chunks first
+  const int s = blockIdx.z;                    // selection row
+  const int unit = a.per_head ? s / a.G : s;   // kv head (with batch)
+  const int qh0 = (a.per_head ? s : s * a.G) + hs * a.heads_per_cta;  // first q head
+  const int nh = a.per_head ? 1 : min(a.heads_per_cta, a.G - hs * a.heads_per_cta);
+  const int bl = l * a.block;
+  const int np = __ldg(a.nplan + (int64_t)s * a.nc + l);
+  const int4* plan = a.plans + ((int64_t)s * a.nc + l) * a.cap;
+  if (np <= 0) return;  // capacity overflow (nplan = -1): reported by the host
+  for (int e = threadIdx.x; e < np && e < 288; e += blockDim.x) s_plan[e] = plan[e];
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 4 * MT);
+    }
+    mbar_init(&o_done, 1);
+    mbar_init(&q_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(&s_tmem, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = s_tmem;
+  const uint32_t sq = smem_u32(smem + SM::q_off);
+  const uint32_t skv = smem_u32(smem + SM::kv_off);
+  const uint32_t sp = smem_u32(smem + SM::p_off);
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer
+    if (lane == 0) {
+      prefetch_tmap(&tmQ);
+      prefetch_tmap(&tmK);
+      prefetch_tmap(&tmV);
+      mbar_expect_tx(&q_full, SM::Q);
+      for (int rg = 0; rg < 2 * MT; ++rg) {
+        const int h = qh0 + (rg < nh ? rg : 0);  // padding row groups repeat a live head
+        const int row = h * a.L + bl;
+        for (int half = 0; half < 2; ++half)
+          tma_load_2d(smem + SM::q_off + (rg >> 1) * 32768 + half * 16384 + (rg & 1) * 8192, &tmQ,
+                      &q_full, half * 64, row);
+      }
+      for (int j = 0; j < np; ++j) {
+        const int st = j % NST;
+        if (j >= NST) mbar_wait(&kv_empty[st], ((j / NST) - 1) & 1);
+        mbar_expect_tx(&kv_full[st], SM::KV);
+        const int row = unit * a.L + s_plan[j].x;
+        unsigned char* kb = smem + SM::kv_off + st * SM::KV;
+        for (int half = 0; half < 2; ++half) {
+          tma_load_2d(kb + half * 8192, &tmK, &kv_full[st], half * 64, row);
+          tma_load_2d(kb + 16384 + half * 8192, &tmV, &kv_full[st], half * 64, row);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer (one thread)
+    if (lane == 0) {
+      constexpr uint32_t idS = umma_idesc_bf16(128, 64, 0, 0);   // Q K^T: both K-major
+      constexpr uint32_t idO = umma_idesc_bf16(128, 128, 0, 1);  // P V: V is MN-major
+      mbar_wait(&q_full, 0);
+      auto issue_s = [&](int j) {
+        const int st = j % NST;
+        mbar_wait(&kv_full[st], (j / NST) & 1);
+        tc_fence_after();
+        const uint32_t kb = skv + st * SM::KV;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k) {
+            const uint64_t ad = umma_sdesc(sq + mt * 32768 + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024);
+            const uint64_t bd = umma_sdesc(kb + (k >> 2) * 8192 + (k & 3) * 32, 16, 1024);
+            umma_bf16(tmem + mt * 128 + (j & 1) * 64, ad, bd, idS, k > 0);
+          }
+        }
+        umma_commit(&s_full[j & 1]);
+      };
+      issue_s(0);
+      for (int j = 0; j < np; ++j) {
+        if (j + 1 < np) issue_s(j + 1);
+        mbar_wait(&p_full[j & 1], (j >> 1) & 1);
+        tc_fence_after();
+        const int st = j % NST;
+        const uint32_t vb = skv + st * SM::KV + 16384;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {  // 64 keys = 4 x 16
+            const uint64_t ad = umma_sdesc(sp + ((j & 1) * MT + mt) * 16384 + k * 32, 16, 1024);
+            const uint64_t bd = umma_sdesc(vb + k * 2048, 8192, 1024);
+            umma_bf16(tmem + MT * 128 + mt * 128, ad, bd, idO, (j > 0 || k > 0) ? 1u : 0u);
+          }
+        }
+        umma_commit(&kv_empty[st]);
+        umma_commit(&o_done);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------ softmax / epilogue warps
+    const int sw = warp - 2;                // 0 .. 4*MT-1
+    const int mt = sw >> 2;                 // M tile
+    const int quad = warp & 3;              // TMEM lane quadrant of this warp
+    const int trow = quad * 32 + lane;      // row within the M tile (= TMEM lane)
+    const int r = mt * 128 + trow;          // row within the CTA tile
+    const int rg = r >> 6;                  // row group = head slot
+    const int i = bl + (r & 63);            // token index of this query row
+    const bool live = rg < nh && i < a.L;
+    const int64_t keep = a.budget < (int64_t)i + 1 ? a.budget : (int64_t)i + 1;
+    const int Ri = (int)(keep - 1);
+    const int dl = i - bl;
+    const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
+    const uint32_t tS = tmem + lane_base + mt * 128;
+    const uint32_t tO = tmem + lane_base + MT * 128 + mt * 128;
+    float m_used = -INFINITY, lsum = 0.f;
+    for (int j = 0; j < np; ++j) {
+      const int4 e = s_plan[j];
+      int lim, self = -1;
+      if (e.w & 2) {
+        lim = max(0, min(Ri - e.z, dl));
+        self = dl;
+      } else {
+        lim = max(0, min(Ri - e.z - ((e.w & 1) ? dl : 0), e.y));
+      }
+      if (!live) {
+        lim = 0;
+        self = -1;
+      }
+      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t v[64];
+      tmem_ld32(tS + (j & 1) * 64, *reinterpret_cast<uint32_t(*)[32]>(v));
+      tmem_ld32(tS + (j & 1) * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+      tmem_wait_ld();
+      float x[64];
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 64; ++c) {
+        const bool ok = c < lim || c == self;
+        x[c] = ok ? __uint_as_float(v[c]) * a.scale_log2 : -INFINITY;
+        mx = fmaxf(mx, x[c]);
+      }
+      // PV of block j-1 done: O is stable and the P buffer of block j-2 is free
+      if (j > 0) mbar_wait(&o_done, (j - 1) & 1);
+      tc_fence_after();
+      // lazy rescale: a row moves its reference max only when its running max
+      // grows by > 2^8 (or on its first finite score, when O holds only
+      // zero-weight terms).  TMEM loads/stores are warp-collective, so the
+      // O rescale runs for the whole warp when any of its rows needs it.
+      float m_new = m_used;
+      if (mx > -INFINITY && (m_used == -INFINITY || mx > m_used + 8.f)) m_new = mx;
+      const bool need = m_used != -INFINITY && m_new != m_used;
+      if (__any_sync(0xffffffffu, need)) {
+        const float f = need ? exp2f(m_used - m_new) : 1.f;
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+          uint32_t o[32];
+          tmem_ld32(tO + cc * 32, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int t = 0; t < 32; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * f);
+          tmem_st32(tO + cc * 32, o);
+        }
+        tmem_wait_st();
+        lsum *= f;
+      }
+      m_used = m_new;
+      const float mref = m_used == -INFINITY ? 0.f : m_used;
+      unsigned char* prow = smem + SM::p_off + ((j & 1) * MT + mt) * 16384 + trow * 128;
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch) {
+        uint32_t w[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const float p0 = exp2f(x[ch * 8 + 2 * t] - mref);
+          const float p1 = exp2f(x[ch * 8 + 2 * t + 1] - mref);
+          lsum += p0 + p1;
+          w[t] = pack_bf16(p0, p1);
+        }
+        *reinterpret_cast<uint4*>(prow + ((ch ^ (trow & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[j & 1]);
+    }
+    mbar_wait(&o_done, (np - 1) & 1);
+    tc_fence_after();
+    const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
+    __nv_bfloat16* orow = a.out + ((int64_t)(qh0 + (rg < nh ? rg : 0)) * a.L + i) * D;
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+      uint32_t o[32];
+      tmem_ld32(tO + cc * 32, o);
+      tmem_wait_ld();
+      if (live) {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          uint4 pk;
+          pk.x = pack_bf16(__uint_as_float(o[8 * t + 0]) * inv, __uint_as_float(o[8 * t + 1]) * inv);
+          pk.y = pack_bf16(__uint_as_float(o[8 * t + 2]) * inv, __uint_as_float(o[8 * t + 3]) * inv);
+          pk.z = pack_bf16(__uint_as_float(o[8 * t + 4]) * inv, __uint_as_float(o[8 * t + 5]) * inv);
+          pk.w = pack_bf16(__uint_as_float(o[8 * t + 6]) * inv, __uint_as_float(o[8 * t + 7]) * inv);
+          *reinterpret_cast<uint4*>(orow + cc * 32 + 8 * t) = pk;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, kTmemCols);
+  }
+}
+
+template <int MT, int NST>
+static int launch_prefill_attn(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+                               const PrefillArgs& a, int S, cudaStream_t st) {
+  using SM = PrefillSmem<MT, NST>;
+  auto kern = prefill_attn_kernel<MT, NST>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::total);
+  if (e != cudaSuccess) {
+    set_error("dhsa_prefill_attn: %s", cudaGetErrorString(e));
+    return DHSA_ECUDA;
+  }
+  dim3 grid((unsigned)a.slices, (unsigned)a.nc, (unsigned)S);
+  kern<<<grid, 64 + 128 * MT, SM::total, st>>>(mq, mk, mv, a);
+  return check_launch("dhsa_prefill_attn");
+}
+
+}  // namespace dhsa
+
+using namespace dhsa;
+
+extern "C" int dhsa_prefill_scores(const double* q_centroids, const double* k_centroids, int U,
+                                   int G, int n_chunks, int D, int agg, double* scores,
+                                   dhsa_stream_t stream) {
+  DHSA_REQUIRE(q_centroids && k_centroids && scores && U >= 1 && G >= 1 && n_chunks >= 1 &&
+                   D >= 1,
+               "dhsa_prefill_scores: bad arguments");
+  DHSA_REQUIRE(agg == DHSA_AGG_NONE || agg == DHSA_AGG_MAX || agg == DHSA_AGG_MEAN,
+               "dhsa_prefill_scores: unknown aggregation %d", agg);
+  const int per_head = agg == DHSA_AGG_NONE;
+  const int S = per_head ? U * G : U;
+  const int t = (n_chunks + 15) / 16;
+  dim3 grid((unsigned)t, (unsigned)t, (unsigned)S);
+  prefill_scores_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(q_centroids, k_centroids, n_chunks,
+                                                                 D, G, per_head, agg, scores);
+  return check_launch("dhsa_prefill_scores");
+}
+
+extern "C" int dhsa_prefill_plan_capacity(int64_t budget, int block) {
+  if (budget < 1 || block < 1) return -1;
+  return (int)((budget - 1 + block - 1) / block) + 2;
+}
+
+extern "C" int dhsa_prefill_plan(const double* scores, int S, int n_chunks, int L, int block,
+                                 int64_t budget, int cap, void* plans, int32_t* nplan,
+                                 dhsa_stream_t stream) {
+  DHSA_REQUIRE(scores && plans && nplan && S >= 1 && n_chunks >= 1 && block >= 1 && L >= 1,
+               "dhsa_prefill_plan: bad arguments");
+  DHSA_REQUIRE(budget >= 1, "budget must be >= 1");
+  DHSA_REQUIRE((int64_t)(n_chunks - 1) * block < L && (int64_t)n_chunks * block >= L,
+               "dhsa_prefill_plan: n_chunks does not match L / block");
+  DHSA_REQUIRE(cap >= 2, "dhsa_prefill_plan: capacity too small");
+  const size_t smem = (size_t)n_chunks * (8 + 4 + 4);
+  DHSA_REQUIRE(smem <= 200 * 1024, "dhsa_prefill_plan: too many chunks (%d)", n_chunks);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(prefill_plan_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) {
+      set_error("dhsa_prefill_plan: %s", cudaGetErrorString(e));
+      return DHSA_ECUDA;
+    }
+  }
+  dim3 grid((unsigned)n_chunks, (unsigned)S);
+  prefill_plan_kernel<<<grid, kPlanThreads, smem, (cudaStream_t)stream>>>(
+      scores, n_chunks, L, block, budget, cap, (int4*)plans, nplan);
+  return check_launch("dhsa_prefill_plan");
+}
+
+extern "C" int dhsa_prefill_attn(const void* q, const void* k, const void* v, int U, int G, int L,
+                                 int D, int block, int agg, int64_t budget, const void* plans,
+                                 const int32_t* nplan, int cap, void* out,
+                                 dhsa_stream_t stream) {
+  DHSA_REQUIRE(q && k && v && plans && nplan && out, "dhsa_prefill_attn: null pointer");
+  DHSA_REQUIRE(D == 128, "dhsa_prefill_attn: head_dim must be 128 (got %d)", D);
+  DHSA_REQUIRE(block == 64, "dhsa_prefill_attn: the tcgen05 tiles need 64-token chunks");
+  DHSA_REQUIRE(U >= 1 && G >= 1 && L >= 1 && cap >= 2 && cap <= 288,
+               "dhsa_prefill_attn: bad shape (plan capacity <= 288)");
+  DHSA_REQUIRE(budget >= 1, "budget must be >= 1");
+  DHSA_REQUIRE(((uintptr_t)q & 15) == 0 && ((uintptr_t)k & 15) == 0 && ((uintptr_t)v & 15) == 0 &&
+                   ((uintptr_t)out & 15) == 0,
+               "dhsa_prefill_attn: pointers must be 16-byte aligned");
+  DHSA_REQUIRE((int64_t)U * G * L < (1ll << 31), "dhsa_prefill_attn: too many rows for TMA");
+  const int per_head = agg == DHSA_AGG_NONE;
+  CUtensorMap mq, mk, mv;
+  int rc = make_tmap_2d(&mq, q, (int64_t)U * G * L, D, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16);
+  if (rc) return rc;
+  rc = make_tmap_2d(&mk, k, (int64_t)U * L, D, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16);
+  if (rc) return rc;
+  rc = make_tmap_2d(&mv, v, (int64_t)U * L, D, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16);
+  if (rc) return rc;
+  PrefillArgs a{};
+  a.plans = (const int4*)plans;
+  a.nplan = nplan;
+  a.cap = cap;
+  a.nc = (L + block - 1) / block;
+  a.L = L;
+  a.block = block;
+  a.budget = budget;
+  a.G = G;
+  a.per_head = per_head;
+  const int gsel = per_head ? 1 : G;
+  a.heads_per_cta = gsel < 4 ? gsel : 4;
+  a.slices = (gsel + a.heads_per_cta - 1) / a.heads_per_cta;
+  a.out = (__nv_bfloat16*)out;
+  a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)D));
+  const int S = per_head ? U * G : U;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (a.heads_per_cta > 2) return launch_prefill_attn<2, 2>(mq, mk, mv, a, S, st);
+  return launch_prefill_attn<1, 4>(mq, mk, mv, a, S, st);
+}

@@ -1,0 +1,151 @@
+"""Batched sparse prefill (config C5) on the tcgen05 tensor cores.
+
+For B sequences of L tokens with Hq query heads sharing Hkv key/value heads
+(G = Hq / Hkv), computes the reference's prefill path for every head —
+prefill_mask (masks.py:143-150: chunk centroids of Q and K, S_c = Q_c K_c^T,
+token-budget Top-K per row with forced self) followed by
+dense_attention(seq, mask) (core.py:98-119) — without ever materialising the
+L x L upsampled score matrix:
+
+  1. ``dhsa_centroids``       Q_c [B*Hq, N_c, D], K_c [B*Hkv, N_c, D] in fp64
+                              (chunk_repr.aggregate_rows, bit-exact);
+  2. ``dhsa_prefill_scores``  S_c per selection row, aggregated over the G
+                              q-heads of a kv group ("max" / "mean",
+                              harness.py:288-306) or per head ("none");
+  3. ``dhsa_prefill_plan``    per (selection row, query chunk) the walk-order
+                              list of selected chunks;
+  4. ``dhsa_prefill_attn``    tcgen05.mma S = Q K^T / O += P V over the planned
+                              64-token KV blocks, per-row masks, online softmax.
+
+Layouts (dense, bf16): q [B, Hq, L, D], k/v [B, Hkv, L, D], out [B, Hq, L, D].
+Static 64-token chunks (chunking.static_boundaries) and D = 128.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+
+
+class SparsePrefill:
+    """Sparse prefill attention with the reference's token budget.
+
+    ``budget`` is the reference's per-row token budget (masks.topk_row); with
+    ``top_k`` blocks it defaults to ``top_k * block + 1`` (K whole blocks +
+    self).  ``agg``: "max" / "mean" (one selection per kv group) or "none"
+    (one selection per q head)."""
+
+    def __init__(self, batch, q_heads, kv_heads, head_dim, seq_len, *, block=64, top_k=16,
+                 budget=None, agg="max", device=None):
+        _lib.require_cuda()
+        if q_heads % kv_heads:
+            raise ValueError("q_heads must be a multiple of kv_heads")
+        if agg not in _lib.AGG:
+            raise ValueError(f"unknown aggregation {agg!r}")
+        if head_dim != 128 or block != 64:
+            raise ValueError("the tcgen05 prefill path needs head_dim 128 and 64-token chunks")
+        self.B, self.Hq, self.Hkv, self.D, self.L = batch, q_heads, kv_heads, head_dim, seq_len
+        self.G = q_heads // kv_heads
+        self.U = batch * kv_heads
+        self.block = block
+        self.budget = int(budget if budget is not None else top_k * block + 1)
+        if self.budget < 1:
+            raise ValueError("budget must be >= 1")
+        self.agg = agg
+        self.nc = (seq_len + block - 1) // block
+        self.S = self.U * self.G if agg == "none" else self.U
+        self.cap = _lib.load().dhsa_prefill_plan_capacity(self.budget, block)
+        if self.cap > 288:
+            raise ValueError("budget too large for the prefill plan (<= 286 blocks per row)")
+        dev = torch.device(device) if device is not None else torch.device("cuda")
+        self.dev = dev
+        kw = dict(device=dev)
+        self.qc = torch.empty(self.U * self.G, self.nc, head_dim, dtype=torch.float64, **kw)
+        self.kc = torch.empty(self.U, self.nc, head_dim, dtype=torch.float64, **kw)
+        self.scores = torch.empty(self.S, self.nc, self.nc, dtype=torch.float64, **kw)
+        self.plans = torch.zeros(self.S, self.nc, self.cap, 4, dtype=torch.int32, **kw)
+        self.nplan = torch.zeros(self.S, self.nc, dtype=torch.int32, **kw)
+        self.plen_q = torch.full((self.U * self.G,), seq_len, dtype=torch.int32, **kw)
+        self.plen_k = torch.full((self.U,), seq_len, dtype=torch.int32, **kw)
+
+    def _check(self, q, k, v):
+        want_q = (self.B, self.Hq, self.L, self.D)
+        want_k = (self.B, self.Hkv, self.L, self.D)
+        for t, w, n in ((q, want_q, "q"), (k, want_k, "k"), (v, want_k, "v")):
+            if tuple(t.shape) != w or t.dtype != torch.bfloat16 or not t.is_contiguous():
+                raise ValueError(f"{n} must be a contiguous bf16 tensor of shape {w}")
+
+    def stages(self, q, k, v, out, stream=None):
+        """The launches as (name, thunk) pairs, in order."""
+        st = _lib.stream_handle(stream)
+        nq, nk = self.U * self.G, self.U
+        lq = _lib.layout(plen=self.plen_q, block=self.block, max_chunks=self.nc)
+        lk = _lib.layout(plen=self.plen_k, block=self.block, max_chunks=self.nc)
+
+        def reps():
+            _lib.call("dhsa_centroids", _lib.BF16, _lib.ptr(q), self.L * self.D, self.D, nq, lq, 1,
+                      _lib.ptr(self.qc), self.nc * self.D, st)
+            _lib.call("dhsa_centroids", _lib.BF16, _lib.ptr(k), self.L * self.D, self.D, nk, lk, 1,
+                      _lib.ptr(self.kc), self.nc * self.D, st)
+
+        def scores():
+            _lib.call("dhsa_prefill_scores", _lib.ptr(self.qc), _lib.ptr(self.kc), self.U, self.G,
+                      self.nc, self.D, _lib.AGG[self.agg], _lib.ptr(self.scores), st)
+
+        def plan():
+            _lib.call("dhsa_prefill_plan", _lib.ptr(self.scores), self.S, self.nc, self.L,
+                      self.block, self.budget, self.cap, _lib.ptr(self.plans),
+                      _lib.ptr(self.nplan), st)
+
+        def attn():
+            _lib.call("dhsa_prefill_attn", _lib.ptr(q), _lib.ptr(k), _lib.ptr(v), self.U, self.G,
+                      self.L, self.D, self.block, _lib.AGG[self.agg], self.budget,
+                      _lib.ptr(self.plans), _lib.ptr(self.nplan), self.cap, _lib.ptr(out), st)
+
+        return [("chunk_reps", reps), ("chunk_scores", scores), ("plan", plan), ("attn", attn)]
+
+    def __call__(self, q, k, v, out=None, stream=None):
+        self._check(q, k, v)
+        if out is None:
+            out = torch.empty_like(q)
+        for _, fn in self.stages(q, k, v, out, stream):
+            fn()
+        return out
+
+    def check_capacity(self):
+        if int(self.nplan.min().item()) < 0:
+            raise _lib.DhsaError("prefill plan capacity exceeded")
+
+    def host_plans(self):
+        """Host copies (plans, nplan) of the last call's plans."""
+        return self.plans.cpu().numpy(), self.nplan.cpu().numpy()
+
+    def row_indices(self, s: int, row: int, host=None):
+        """Token indices row `row` of selection row `s` attends to, decoded
+        from the plan (for tests and inspection; pass ``host_plans()`` to
+        avoid a device copy per call)."""
+        import numpy as np
+
+        plans, nplan = host if host is not None else self.host_plans()
+        l = row // self.block
+        n = int(nplan[s, l])
+        ent = plans[s, l, :n]
+        R = min(self.budget, row + 1) - 1
+        d = row - l * self.block
+        out = [row]
+        for start, ln, w, fl in ent:
+            if fl & 2:
+                lim = max(0, min(R - w, d))
+            else:
+                lim = max(0, min(R - w - (d if fl & 1 else 0), ln))
+            out.extend(range(start, start + lim))
+        return np.sort(np.array(out, dtype=np.int64))
+
+    def flops(self) -> float:
+        """Algorithmic flops: 4 * sum_i min(i+1, budget) * D per q head
+        (QK^T and PV over the selected keys)."""
+        L, b = self.L, self.budget
+        m = min(L, b)
+        tot = m * (m + 1) // 2 + (L - m) * b
+        return 4.0 * tot * self.D * self.Hq * self.B

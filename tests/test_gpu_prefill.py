@@ -1,0 +1,117 @@
+"""GPU parity of the tcgen05 sparse prefill (config C5's path) against the
+CPU oracle: the per-row index sets the plans encode must equal the oracle's
+prefill rows (masks.prefill_mask semantics: topk_row on the upsampled row,
+head-aggregated S_c for GQA groups) index-for-index, and the attention output
+must match the float64 row body (core.py:113-118) within 2e-2 of max|o_ref|
+per (sequence, head) — the bf16 tolerance of the north star."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import dhsa_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL_BF16 = 2e-2
+
+
+def _inputs(B, Hq, Hkv, L, D, seed, kind="normal"):
+    rng = np.random.default_rng(seed)
+
+    def draw(*shape):
+        if kind == "int":
+            return rng.integers(-3, 4, size=shape).astype(np.float32)
+        return rng.standard_normal(shape, dtype=np.float32)
+
+    q, k, v = draw(B, Hq, L, D), draw(B, Hkv, L, D), draw(B, Hkv, L, D)
+    if kind == "wide":  # large logits: exercises the online-softmax rescaling
+        q *= 8.0
+    if kind == "ties":
+        k[:, :, 128:192] = k[:, :, 0:64]
+    t = {n: torch.from_numpy(np.ascontiguousarray(x)).bfloat16() for n, x in
+         dict(q=q, k=k, v=v).items()}
+    host = {n: x.double().numpy() for n, x in t.items()}
+    return t, host
+
+
+def _run(B, Hq, Hkv, L, top_k=None, budget=None, agg="max", seed=0, kind="normal",
+         check_rows=None, check_out=True):
+    from paper_2510_24606_b200.prefill import SparsePrefill
+
+    D = 128
+    G = Hq // Hkv
+    t, host = _inputs(B, Hq, Hkv, L, D, seed, kind)
+    pf = SparsePrefill(B, Hq, Hkv, D, L, top_k=top_k or 4, budget=budget, agg=agg)
+    out = pf(t["q"].cuda(), t["k"].cuda(), t["v"].cuda())
+    torch.cuda.synchronize()
+    pf.check_capacity()
+    o = out.double().cpu().numpy()
+    bounds = O.static_grid(L, 64)
+    hp = pf.host_plans()
+    worst = 0.0
+    for b in range(B):
+        for h in range(Hkv):
+            u = b * Hkv + h
+            qh = host["q"][b, h * G:(h + 1) * G]
+            kh = np.repeat(host["k"][b, h][None], G, axis=0)
+            if agg == "none":
+                per = [O.prefill_rows(qh[j], kh[j], bounds, pf.budget) for j in range(G)]
+            else:
+                rows = O.prefill_rows(qh, kh, bounds, pf.budget, agg=agg)
+                per = [rows] * G
+            check = range(L) if check_rows is None else check_rows
+            for j in range(G):
+                s = u * G + j if agg == "none" else u
+                for i in check:
+                    got = pf.row_indices(s, i, hp)
+                    assert np.array_equal(got, per[j][i]), (b, h, j, i, len(got), len(per[j][i]))
+            if check_out:
+                for j in range(G):
+                    ref = O.attend_rows(qh[j], host["k"][b, h], host["v"][b, h], per[j])
+                    err = np.abs(o[b, h * G + j] - ref).max() / np.abs(ref).max()
+                    worst = max(worst, err)
+    return worst
+
+
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+def test_prefill_group_sizes(G):
+    worst = _run(B=1, Hq=2 * G, Hkv=2, L=1024, top_k=4, agg="max", seed=G,
+                 check_rows=range(0, 1024, 7))
+    assert worst <= TOL_BF16, worst
+
+
+@pytest.mark.parametrize("agg", ["mean", "none"])
+def test_prefill_aggregations(agg):
+    worst = _run(B=2, Hq=8, Hkv=2, L=768, top_k=3, agg=agg, seed=11,
+                 check_rows=range(0, 768, 5))
+    assert worst <= TOL_BF16, worst
+
+
+@pytest.mark.parametrize("budget", [1, 2, 63, 64, 100, 257, 5000])
+def test_prefill_budgets(budget):
+    """Self only, cut chunks (K*64 and odd budgets), more than the context."""
+    worst = _run(B=1, Hq=4, Hkv=1, L=640, budget=budget, agg="max", seed=budget,
+                 check_rows=range(640))
+    assert worst <= TOL_BF16, worst
+
+
+def test_prefill_ragged_length():
+    """L not a multiple of 64: the last chunk is short."""
+    worst = _run(B=1, Hq=4, Hkv=1, L=1000, top_k=5, agg="max", seed=4, check_rows=range(1000))
+    assert worst <= TOL_BF16, worst
+
+
+@pytest.mark.parametrize("kind", ["ties", "int", "wide"])
+def test_prefill_ties(kind):
+    """Exact score ties (duplicated blocks / small integers): lower chunk
+    index first, as the reference's stable argsort."""
+    worst = _run(B=1, Hq=4, Hkv=1, L=512, top_k=3, agg="max", seed=9, kind=kind,
+                 check_rows=range(512))
+    assert worst <= TOL_BF16, worst
+
+
+def test_prefill_4k_topk16():
+    worst = _run(B=1, Hq=8, Hkv=2, L=4096, top_k=16, agg="max", seed=21,
+                 check_rows=range(0, 4096, 31))
+    assert worst <= TOL_BF16, worst
