@@ -130,6 +130,27 @@ int dhsa_attn(int dtype, const void* q, const void* k_cache, const void* v_cache
               void* workspace, int32_t* counters, int32_t* ready,
               dhsa_stream_t stream);
 
+/* Persistent, dynamically balanced bf16 variant of dhsa_attn: a grid of
+ * resident CTAs (occupancy x SMs) pulls chunks of the virtual tile space
+ * items x tiles_hint from a device counter; each CTA's TMA ring streams
+ * everything it pulls, ring entries carrying their metadata; the tiles of an
+ * item one CTA processed end in an (m, l, acc) record and the segment that
+ * completes the item's tile count merges them.  Tiles beyond tiles_hint go to
+ * whoever pulls the item's last slot, so the result does not depend on the
+ * hint (only the balance does).  Writes out (bf16) or, when records != NULL,
+ * the unnormalised per-row records of dhsa_attn_partials.
+ * workspace: dhsa_attn_stream_workspace_size bytes; counters:
+ * int32[dhsa_attn_stream_counters(items)] zero at rest (re-armed in-kernel);
+ * ready as in dhsa_attn, except that the flags are re-armed by the next
+ * step's dhsa_decode_step_bf16 rather than by the attention. */
+int dhsa_attn_stream_counters(int items);
+int64_t dhsa_attn_stream_workspace_size(int items, int GH, int D);
+int dhsa_attn_stream(const void* q, const void* k_cache, const void* v_cache,
+                     int64_t cache_unit_stride, int64_t cache_rows, int items, int items_per_unit,
+                     int GH, int D, const int32_t* tiles, int64_t tile_cap,
+                     const int32_t* ntiles, int tiles_hint, void* out, float* records,
+                     void* workspace, int32_t* counters, int32_t* ready, dhsa_stream_t stream);
+
 /* gen_count[u] += 1 for all units (masks.py:236). */
 int dhsa_decode_advance(int32_t* gen_count, int U, dhsa_stream_t stream);
 

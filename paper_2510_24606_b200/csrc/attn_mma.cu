@@ -18,6 +18,7 @@
 // are masked; the KV cache is finite everywhere (zero-initialised), so the
 // masked rows contribute exactly 0.
 #include "attn_common.cuh"
+#include "attn_tile.cuh"
 #include "capi.cuh"
 
 
@@ -30,11 +31,8 @@ __global__ __launch_bounds__(160) void attn_mma_kernel(
     const int32_t* __restrict__ tiles, int64_t tile_cap, const int32_t* __restrict__ ntiles,
     int splits, __nv_bfloat16* __restrict__ out, void* ws, int32_t* counters, float scale_log2,
     int32_t* ready, float* __restrict__ rec_out) {
-  constexpr int NB = D / 64;                  // 128-byte column boxes per row
-  constexpr int BOX = 64 * 128;               // one box: 64 token rows x 128 B
-  constexpr int STAGE_BYTES = 2 * NB * BOX;   // K + V
-  constexpr int KS = D / 16;                  // k-steps of QK^T
-  constexpr int NT = D / 8;                   // n-tiles of PV
+  using T = DecodeTile<D>;
+  constexpr int NB = T::NB, BOX = T::BOX, STAGE_BYTES = T::STAGE_BYTES;
 
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem =
@@ -65,9 +63,9 @@ __global__ __launch_bounds__(160) void attn_mma_kernel(
   __syncthreads();
 
   float m = -INFINITY, l = 0.f;
-  float o[NT][4];
+  float o[T::NT][4];
 #pragma unroll
-  for (int j = 0; j < NT; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+  for (int j = 0; j < T::NT; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
 
   if (warp == 4) {
     // ---------------- TMA producer ----------------
@@ -90,85 +88,13 @@ __global__ __launch_bounds__(160) void attn_mma_kernel(
     }
   } else {
     // ---------------- consumers ----------------
-    const int hrow = lane >> 2;  // head row of the A / C fragments
-    uint32_t qa[KS][2];
-    {
-      const bool live = hrow < GH;
-      const __nv_bfloat16* qrow = q + ((int64_t)item * GH + (live ? hrow : 0)) * D;
-#pragma unroll
-      for (int ks = 0; ks < KS; ++ks) {
-        const int k0 = ks * 16 + 2 * (lane & 3);
-        qa[ks][0] = live ? *reinterpret_cast<const uint32_t*>(qrow + k0) : 0u;
-        qa[ks][1] = live ? *reinterpret_cast<const uint32_t*>(qrow + k0 + 8) : 0u;
-      }
-    }
-    // per-lane ldmatrix row/chunk selectors
-    const int mi = lane >> 3, r8 = lane & 7;
-    const int tok_k = warp * 16 + 8 * (mi >> 1) + r8;  // K: matrix (nt, khalf)
-    const int tok_v = warp * 16 + 8 * (mi & 1) + r8;   // V: matrix (tokhalf, ntile)
-
+    uint32_t qa[T::KS][2];
+    T::load_q(q, item, GH, lane, qa);
     for (int i = 0; i < n; ++i) {
       const int s = i % STAGES;
       mbar_wait(&full_bar[s], (i / STAGES) & 1);
       const int count = __ldcg(tl + 2 * i + 1);
-      if (warp * 16 < count) {
-        const uint32_t kb = smem_u32(smem + s * STAGE_BYTES);
-        const uint32_t vb = kb + NB * BOX;
-        float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-#pragma unroll
-        for (int ks = 0; ks < KS; ++ks) {
-          const int dch = 2 * ks + (mi & 1);
-          const uint32_t addr =
-              kb + (dch >> 3) * BOX + tok_k * 128 + (((dch & 7) ^ (tok_k & 7)) << 4);
-          uint32_t b0, b1, b2, b3;
-          ldsm_x4(addr, b0, b1, b2, b3);
-          mma_bf16(sc[0], qa[ks][0], 0u, qa[ks][1], 0u, b0, b1);
-          mma_bf16(sc[1], qa[ks][0], 0u, qa[ks][1], 0u, b2, b3);
-        }
-        // scores of head `hrow` for tokens warp*16 + 8*nt + 2*(lane&3) + {0,1}
-        float p[2][2];
-        float tmax = -INFINITY;
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int tok = warp * 16 + 8 * nt + 2 * (lane & 3) + e;
-            const float v = tok < count ? sc[nt][e] * scale_log2 : -INFINITY;
-            p[nt][e] = v;
-            tmax = fmaxf(tmax, v);
-          }
-        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
-        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
-        const float mn = fmaxf(m, tmax);
-        const float corr = exp2f(m - mn);
-        float psum = 0.f;
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            p[nt][e] = exp2f(p[nt][e] - mn);
-            psum += p[nt][e];
-          }
-        l = l * corr + psum;
-        m = mn;
-#pragma unroll
-        for (int j = 0; j < NT; ++j) {
-          o[j][0] *= corr;
-          o[j][1] *= corr;
-        }
-        const uint32_t pa0 = pack_bf16(p[0][0], p[0][1]);
-        const uint32_t pa2 = pack_bf16(p[1][0], p[1][1]);
-#pragma unroll
-        for (int np = 0; np < NT / 2; ++np) {
-          const int dch = 2 * np + (mi >> 1);
-          const uint32_t addr =
-              vb + (dch >> 3) * BOX + tok_v * 128 + (((dch & 7) ^ (tok_v & 7)) << 4);
-          uint32_t b0, b1, b2, b3;
-          ldsm_x4_t(addr, b0, b1, b2, b3);
-          mma_bf16(o[2 * np], pa0, 0u, pa2, 0u, b0, b1);
-          mma_bf16(o[2 * np + 1], pa0, 0u, pa2, 0u, b2, b3);
-        }
-      }
+      T::update(smem_u32(smem + s * STAGE_BYTES), count, warp, lane, qa, scale_log2, m, l, o);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_bar[s]);
     }
@@ -177,39 +103,14 @@ __global__ __launch_bounds__(160) void attn_mma_kernel(
   }
   __syncthreads();
   // All TMA traffic has been consumed: the stage ring is reused for the merge.
-  const int rec = D + 2;
   float* red = reinterpret_cast<float*>(smem);  // [4 warps][GH][D+2]
-  if (warp < 4) {
-    const int h = lane >> 2;
-    if (h < GH) {
-      float* r = red + (warp * GH + h) * rec;
-      if ((lane & 3) == 0) {
-        r[0] = m;
-        r[1] = l;
-      }
-#pragma unroll
-      for (int j = 0; j < NT; ++j) {
-        r[2 + j * 8 + 2 * (lane & 3)] = o[j][0];
-        r[2 + j * 8 + 2 * (lane & 3) + 1] = o[j][1];
-      }
-    }
-  }
+  if (warp < 4) T::warp_record(red, warp, lane, GH, m, l, o);
   __syncthreads();
   const bool direct = (splits == 1);
   for (int hd = threadIdx.x; hd < GH * D; hd += blockDim.x) {
     const int h = hd / D, d = hd - h * D;
-    float mstar = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) mstar = fmaxf(mstar, red[(w * GH + h) * rec]);
-    float lsum = 0.f, a = 0.f;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const float* r = red + (w * GH + h) * rec;
-      if (r[0] == -INFINITY) continue;
-      const float wgt = exp2f(r[0] - mstar);
-      lsum += wgt * r[1];
-      a += wgt * r[2 + d];
-    }
+    float mstar, lsum, a;
+    combine4<D>(red, GH, h, d, mstar, lsum, a);
     if (direct && rec_out) {  // unnormalised record for a cross-GPU merge
       float* r = rec_out + ((int64_t)item * GH + h) * (D + 2);
       if (d == 0) {

@@ -170,6 +170,19 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
 
+// ----------------------------------------------------- debug timestamps --
+// DHSA_DEBUG_TIMING=<device address of a uint64 buffer> makes the decode
+// kernels record %globaltimer at phase boundaries (tools/select_phases.py):
+// select CTAs at [16 u + k], sketch CTAs at kDbgSketch + 2 b (+1 = end),
+// attention CTAs at kDbgAttn + 4 b (+1 first tile, +2 end).
+constexpr int kDbgSketch = 65536;
+constexpr int kDbgAttn = 131072;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 // ------------------------------------------ programmatic launch + flags --
 // Let the next kernel in the stream (launched with programmatic stream
 // serialization) start once every CTA of this grid has executed this.

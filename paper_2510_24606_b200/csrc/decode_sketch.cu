@@ -75,7 +75,8 @@ struct SketchArgs {
   int smem_select;
   int n_max;
   int advance;
-  int32_t* ready;           // [items] select -> attention flags (zero at rest) or null
+  int32_t* ready;           // [items] select -> attention flags (zeroed by the sketch kernel) or null
+  int n_units;
   unsigned long long* dbg;  // optional per-CTA phase timestamps (DHSA_DEBUG_TIMING)
   // sequence-sharded split-KV mode (dhsa_decode_candidates_bf16): this shard
   // holds global prompt chunks [chunk_offset, chunk_offset + nchunks); the
@@ -89,11 +90,6 @@ struct SketchArgs {
   int cand_cap;
 };
 
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
 #define DBG_T(k) \
   if (a.dbg && threadIdx.x == 0) a.dbg[blockIdx.x * 16 + (k)] = gtimer()
 
@@ -166,7 +162,17 @@ __global__ __launch_bounds__(kTcThreads) void sketch_score_kernel(
     }
     fence_barrier_init();
   }
+  if (a.ready) {
+    // re-arm the select -> attention flags of this step before any select CTA
+    // can launch (the previous step's attention has completed: this kernel is
+    // not launched programmatically)
+    const int items = AGG == DHSA_AGG_NONE ? a.n_units * G : a.n_units;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < items; i += gridDim.x * blockDim.x)
+      a.ready[i] = 0;
+    __threadfence();
+  }
   __syncthreads();
+  if (a.dbg && threadIdx.x == 0) a.dbg[kDbgSketch + 2 * blockIdx.x] = gtimer();
   pdl_trigger();  // the select kernel may launch (and run its prologue) right away
   // contiguous slice range per CTA; (unit, first chunk) advanced incrementally
   const int spu = a.slices_per_unit;
@@ -297,6 +303,7 @@ __global__ __launch_bounds__(kTcThreads) void sketch_score_kernel(
       }
     }
   }
+  if (a.dbg && threadIdx.x == 0) a.dbg[kDbgSketch + 2 * blockIdx.x + 1] = gtimer();
 }
 
 // --------------------------------------------------------------- selection --
@@ -838,6 +845,7 @@ static int decode_step_impl(
   a.n_max = layout.max_chunks + 1;
   a.advance = advance;
   a.ready = ready;
+  a.n_units = U;
   if (shard) {
     DHSA_REQUIRE(cand && cand_cap >= 1 && cand_stride >= (int64_t)sizeof(SplitCand) * (cand_cap + 1) &&
                      cand_stride % 8 == 0,

@@ -169,11 +169,12 @@ template <int MT, int NST>
 struct PrefillSmem {
   static constexpr int Q = MT * 2 * 16384;         // [mt][D half][128 rows][128 B]
   static constexpr int KV = 2 * 2 * 8192;           // K [half][64][128B] + V [half][64][128B]
-  static constexpr int P = MT * 16384;             // one P buffer: [mt][128 rows][128 B]
+  static constexpr int P = MT * 16384;             // the P buffer: [mt][128 rows][128 B]
   static constexpr int q_off = 0;
   static constexpr int kv_off = Q;
   static constexpr int p_off = Q + NST * KV;
-  static constexpr int total = p_off + 2 * P + 1024;  // + alignment slack
+  // one P buffer: P_j is written only after PV_{j-1} completed (o_done)
+  static constexpr int total = p_off + P + 1024;  // + alignment slack
 };
 
 template <int MT, int NST>
@@ -285,7 +286,7 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_kernel(
         for (int mt = 0; mt < MT; ++mt) {
 #pragma unroll
           for (int k = 0; k < 4; ++k) {  // 64 keys = 4 x 16
-            const uint64_t ad = umma_sdesc(sp + ((j & 1) * MT + mt) * 16384 + k * 32, 16, 1024);
+            const uint64_t ad = umma_sdesc(sp + mt * 16384 + k * 32, 16, 1024);
             const uint64_t bd = umma_sdesc(vb + k * 2048, 8192, 1024);
             umma_bf16(tmem + MT * 128 + mt * 128, ad, bd, idO, (j > 0 || k > 0) ? 1u : 0u);
           }
@@ -339,7 +340,7 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_kernel(
         x[c] = ok ? __uint_as_float(v[c]) * a.scale_log2 : -INFINITY;
         mx = fmaxf(mx, x[c]);
       }
-      // PV of block j-1 done: O is stable and the P buffer of block j-2 is free
+      // PV of block j-1 done: O is stable and the P buffer is free
       if (j > 0) mbar_wait(&o_done, (j - 1) & 1);
       tc_fence_after();
       // lazy rescale: a row moves its reference max only when its running max
@@ -365,7 +366,7 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_kernel(
       }
       m_used = m_new;
       const float mref = m_used == -INFINITY ? 0.f : m_used;
-      unsigned char* prow = smem + SM::p_off + ((j & 1) * MT + mt) * 16384 + trow * 128;
+      unsigned char* prow = smem + SM::p_off + mt * 16384 + trow * 128;
 #pragma unroll
       for (int ch = 0; ch < 8; ++ch) {
         uint32_t w[4];
@@ -518,6 +519,6 @@ extern "C" int dhsa_prefill_attn(const void* q, const void* k, const void* v, in
   a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)D));
   const int S = per_head ? U * G : U;
   cudaStream_t st = (cudaStream_t)stream;
-  if (a.heads_per_cta > 2) return launch_prefill_attn<2, 2>(mq, mk, mv, a, S, st);
-  return launch_prefill_attn<1, 4>(mq, mk, mv, a, S, st);
+  if (a.heads_per_cta > 2) return launch_prefill_attn<2, 3>(mq, mk, mv, a, S, st);
+  return launch_prefill_attn<1, 5>(mq, mk, mv, a, S, st);
 }

@@ -51,7 +51,7 @@ class SparseDecoder:
 
     def __init__(self, batch, q_heads, kv_heads, head_dim, max_len, *, block=64, top_k=64,
                  budget=None, dtype=torch.bfloat16, agg="max", tile=64, splits=None,
-                 device=None, scoring=None):
+                 device=None, scoring=None, attn_mode=None):
         _lib.require_cuda()
         if q_heads % kv_heads:
             raise ValueError("q_heads must be a multiple of kv_heads")
@@ -90,10 +90,21 @@ class SparseDecoder:
         self.ntiles = torch.zeros(self.items, dtype=torch.int32, **kw)
         tiles_per_item = math.ceil(r / self.tile) + 2
         self.splits = int(splits) if splits else default_splits(self.items, tiles_per_item)
-        nbytes = _lib.load().dhsa_attn_workspace_size(self.code, self.items, self.GH, head_dim,
-                                                      self.splits)
+        # attention: "stream" (persistent stream-K grid, bf16) or "split"
+        # (a fixed split-KV factor per item, every dtype)
+        bf16_tc = dtype == torch.bfloat16 and head_dim in (64, 128)
+        self.attn_mode = attn_mode or ("stream" if bf16_tc and not splits else "split")
+        if self.attn_mode == "stream" and not bf16_tc:
+            raise ValueError("stream attention needs bf16 and D in {64, 128}")
+        self.tiles_hint = min(self.tile_cap, tiles_per_item + 1)
+        if self.attn_mode == "stream":
+            nbytes = _lib.load().dhsa_attn_stream_workspace_size(self.items, self.GH, head_dim)
+        else:
+            nbytes = _lib.load().dhsa_attn_workspace_size(self.code, self.items, self.GH,
+                                                          head_dim, self.splits)
         self.ws = torch.empty(max(nbytes, 8), dtype=torch.uint8, **kw)
-        self.counters = torch.zeros(self.items, dtype=torch.int32, **kw)
+        ncnt = max(self.items, _lib.load().dhsa_attn_stream_counters(self.items))
+        self.counters = torch.zeros(ncnt, dtype=torch.int32, **kw)
         self.max_prompt = 0
         self.max_chunks = 0
         self.steps = 0
@@ -194,7 +205,18 @@ class SparseDecoder:
 
         return [("decode_score", score), ("decode_select", select), attn, ("advance", advance)]
 
-    def _attn(self, q, out, st):
+    def _attn(self, q, out, st, records=None):
+        ready = _lib.ptr(self.ready) if self.scoring == "sketch" else 0
+        if self.attn_mode == "stream":
+            _lib.call("dhsa_attn_stream", _lib.ptr(q), _lib.ptr(self.k_cache),
+                      _lib.ptr(self.v_cache), self.L_cap * self.D, self.L_cap, self.items,
+                      self.G if self.per_head else 1, self.GH, self.D, _lib.ptr(self.tiles),
+                      self.tile_cap, _lib.ptr(self.ntiles), self.tiles_hint, _lib.ptr(out),
+                      _lib.ptr(records), _lib.ptr(self.ws), _lib.ptr(self.counters),
+                      ready if records is None else 0, st)
+            return
+        if records is not None:
+            raise ValueError("records need the stream attention mode")
         _lib.call("dhsa_attn", self.code, _lib.ptr(q), _lib.ptr(self.k_cache),
                   _lib.ptr(self.v_cache), self.L_cap * self.D, self.L_cap, self.items,
                   self.G if self.per_head else 1, self.GH, self.D, _lib.ptr(self.tiles),

@@ -96,7 +96,7 @@ class SplitKVShard:
 
     def __init__(self, batch, q_heads, kv_heads, head_dim, prompt_len, *, rank, world,
                  block=64, top_k=64, budget=None, agg="max", max_new=1024, tile=64,
-                 splits=None, device=None):
+                 splits=None, device=None, attn_mode=None):
         self.rank, self.world = int(rank), int(world)
         self.block = int(block)
         self.total_prompt = int(prompt_len)
@@ -108,7 +108,8 @@ class SplitKVShard:
         cap_len = self.local_len + (int(max_new) if self.owns_tail else 0) + 1
         self.dec = SparseDecoder(batch, q_heads, kv_heads, head_dim, cap_len, block=block,
                                  top_k=top_k, budget=budget, dtype=torch.bfloat16, agg=agg,
-                                 tile=tile, splits=splits, device=device, scoring="sketch")
+                                 tile=tile, splits=splits, device=device, scoring="sketch",
+                                 attn_mode=attn_mode)
         d = self.dec
         self.B, self.Hq, self.Hkv, self.D, self.G = d.B, d.Hq, d.Hkv, d.D, d.G
         self.budget = d.budget
@@ -160,7 +161,11 @@ class SplitKVShard:
                   _lib.ptr(d.ntiles), 1, _lib.stream_handle(stream))
 
     def attend(self, q, stream=None):
+        """Attention over this shard's tiles -> (m, l, acc) records."""
         d = self.dec
+        if d.attn_mode == "stream":
+            d._attn(q, None, _lib.stream_handle(stream), records=self.rec)
+            return
         _lib.call("dhsa_attn_partials", _lib.ptr(q), _lib.ptr(d.k_cache), _lib.ptr(d.v_cache),
                   d.L_cap * d.D, d.L_cap, d.items, self.items_per_unit, d.GH, d.D,
                   _lib.ptr(d.tiles), d.tile_cap, _lib.ptr(d.ntiles), d.splits,

@@ -183,3 +183,19 @@ def test_sketch_c3_shape_sampled_units():
     worst = run_and_check(dec, t, host, P, steps, "max", check_units=list(range(16)),
                           check_out=True)
     assert worst <= 2e-2
+
+
+@pytest.mark.parametrize("mode,hint", [("split", None), ("stream", None), ("stream", 2),
+                                       ("stream", 1000)])
+def test_attention_modes(mode, hint):
+    """Persistent stream-K attention (any tiles_hint: too small hands the
+    excess to the last segment, too large leaves idle slots) and the fixed
+    split-KV kernel give the same, in-tolerance outputs."""
+    B, Hq, Hkv, D, P, steps = 3, 16, 4, 128, 3000, 3
+    t, host = make_inputs(B, Hq, Hkv, D, P, steps, torch.bfloat16, seed=17)
+    dec = _dec(batch=B, q_heads=Hq, kv_heads=Hkv, head_dim=D, max_len=P + steps, block=64,
+               top_k=8, dtype=torch.bfloat16, agg="max", attn_mode=mode)
+    if hint is not None:
+        dec.tiles_hint = hint
+    worst = run_and_check(dec, t, host, P, steps, "max")
+    assert worst <= TOL[torch.bfloat16], worst

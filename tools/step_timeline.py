@@ -1,0 +1,90 @@
+"""Timeline of one C3 decode step replayed from a CUDA graph: per-CTA
+%globaltimer stamps of the sketch stream, select and attention kernels
+(DHSA_DEBUG_TIMING, see common.cuh), printed relative to the earliest sketch
+CTA start.  Usage: python tools/step_timeline.py [B] [context]."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+B = int(sys.argv[1]) if len(sys.argv) > 1 else 32
+L = int(sys.argv[2]) if len(sys.argv) > 2 else 131072
+Hq, Hkv, D = 32, 8, 128
+dbg = torch.zeros(262144, dtype=torch.int64, device="cuda")
+os.environ["DHSA_DEBUG_TIMING"] = str(dbg.data_ptr())
+from paper_2510_24606_b200.decode import SparseDecoder  # noqa: E402
+
+dec = SparseDecoder(B, Hq, Hkv, D, L + 64, block=64, top_k=64, dtype=torch.bfloat16, agg="max")
+g = torch.Generator(device="cuda")
+g.manual_seed(0)
+for t in (dec.k_cache, dec.v_cache):
+    t[:, :, :L].normal_(generator=g)
+dec.prefill(dec.k_cache, dec.v_cache, prompt_len=L)
+q = torch.randn(B, Hq, D, device="cuda", generator=g).bfloat16()
+k = torch.randn(B, Hkv, D, device="cuda", generator=g).bfloat16()
+v = torch.randn(B, Hkv, D, device="cuda", generator=g).bfloat16()
+out = torch.empty(B, Hq, D, dtype=torch.bfloat16, device="cuda")
+dec.step(q, k, v, out=out)
+torch.cuda.synchronize()
+s = torch.cuda.Stream()
+gr = torch.cuda.CUDAGraph()
+with torch.cuda.graph(gr, stream=s):
+    dec.launch(q, k, v, out, stream=s)
+for _ in range(5):
+    gr.replay()
+torch.cuda.synchronize()
+dbg.zero_()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+gr.replay()
+e1.record()
+torch.cuda.synchronize()
+t = dbg.cpu().numpy().astype(np.int64)
+sk = t[65536:65536 + 2 * 1024].reshape(-1, 2)
+sk = sk[sk[:, 0] > 0]
+t0 = sk[:, 0].min()
+sel = t[:dec.U * 16].reshape(dec.U, 16)
+at = t[131072:131072 + 4 * 2048].reshape(-1, 4)
+ep = t[131072 + 8192:131072 + 8192 + 4 * 2048].reshape(-1, 4)
+live = at[:, 0] > 0
+at = at[live]
+ep = ep[live]
+
+
+def show(name, col):
+    col = col[col > 0]
+    if len(col):
+        r = (col - t0) / 1e3
+        print(f"{name:28s} min {r.min():8.2f}  med {np.median(r):8.2f}  max {r.max():8.2f} us  (n={len(r)})")
+
+
+print(f"graph replay (events): {e0.elapsed_time(e1) * 1e3:.1f} us")
+show("sketch CTA start", sk[:, 0])
+show("sketch CTA end", sk[:, 1])
+for k_, n in [(0, "select start"), (1, "select after pdl_wait"), (3, "select after radix"),
+              (4, "select classified"), (7, "select emitted"), (8, "select end")]:
+    show(n, sel[:, k_])
+show("attn CTA start", at[:, 0])
+show("attn first tile", at[:, 1])
+show("attn CTA end", at[:, 2])
+print("uncertain chunks per unit: median", np.median(sel[:, 15]), "max", sel[:, 15].max())
+ends = (at[:, 2] - t0) / 1e3
+ntl = at[:, 3] & 0xFFFFFFFF
+smid = at[:, 3] >> 32
+order = np.argsort(ends)
+print("tiles per CTA: min", ntl.min(), "med", np.median(ntl), "max", ntl.max(), "sum", ntl.sum())
+print("slowest CTAs (end us, tiles, first-tile us, start us):")
+for i in order[-8:]:
+    peers = [int(j) for j in np.nonzero(smid == smid[i])[0] if j != i]
+    print(f"  cta {i:4d} sm {smid[i]:3d} end {ends[i]:8.2f} tiles {ntl[i]:4d} first {(at[i, 1] - t0) / 1e3:8.2f} "
+          f"start {(at[i, 0] - t0) / 1e3:8.2f} peers {[(p, round(float(ends[p]), 1), int(ntl[p])) for p in peers]}")
+print("fastest:", [(int(i), round(float(ends[i]), 1), int(ntl[i])) for i in order[:5]])
+per_sm = {}
+for i in range(len(smid)):
+    per_sm.setdefault(int(smid[i]), []).append(i)
+print("CTAs per SM histogram:", np.bincount([len(v) for v in per_sm.values()]))
+slow_sms = sorted(per_sm, key=lambda k: -max(ends[i] for i in per_sm[k]))[:12]
+print("slowest SMs:", slow_sms)
