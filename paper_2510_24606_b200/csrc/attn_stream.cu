@@ -123,11 +123,12 @@ __global__ __launch_bounds__(192, 2) void attn_stream_kernel(const __grid_consta
       if (it >= STAGES) mbar_wait(&empty_bar[st], ((it / STAGES) + 1) & 1);
       return st;
     };
+    int knext = 0;
+    if (lane == 0) knext = atomicAdd(pull, 1);
     for (;;) {
-      int k = 0;
-      if (lane == 0) k = atomicAdd(pull, 1);
-      k = __shfl_sync(0xffffffffu, k, 0);
+      const int k = __shfl_sync(0xffffffffu, knext, 0);
       if (k >= total) break;
+      if (lane == 0) knext = atomicAdd(pull, 1);  // the next pull, in flight meanwhile
       const int item = k / a.nseg, j = k - item * a.nseg;
       int nt = 0;
       if (lane == 0) {
