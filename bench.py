@@ -348,7 +348,7 @@ def run_gpu(args):
                    "selection": "group-shared max over q-heads", "parallelism": f"dp{world}",
                    "l2": "inputs larger than L2 (centroids 537 MB + selected KV 537 MB per step)",
                    "graphs": f"one CUDA graph per step ({dec.kernels_per_step} kernels)",
-                   "scoring": dec.scoring},
+                   "scoring": dec.scoring, "attention": dec.attn_mode},
         "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "algorithmic_bytes": kern_bytes[dominant]},
@@ -361,10 +361,11 @@ def run_gpu(args):
                 "path": "SparseDecoder.step (ctypes C-ABI) with pinned host q/k/v -> o"},
         "gpu_launches": dec.kernels_per_step * S,
         "clocks": clk.summary(),
-        "splits": dec.splits,
+        "splits": dec.splits if dec.attn_mode == "split" else None,
     }
     if rank == 0 and world == 1 and not args.no_cpu:
-        result["cpu_baseline"] = cpu_baseline(name, units_sample=args.cpu_units)
+        # ~10-20 s of host CPU work: 16+ units x 8 decode steps
+        result["cpu_baseline"] = cpu_baseline(name, units_sample=args.cpu_units or 64, steps=8)
     if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:
@@ -559,10 +560,11 @@ def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    name = args.config
+    name = args.config if args.config in CONFIGS else "C3"
     B = CONFIGS[name][0]
     vals = []
     cb = None
+    # each step: one bounded sample (16 units x 1 decode step) of the workload
     for i in range(args.warmup_ref + args.steps_ref):
         cb = cpu_baseline(name, units_sample=args.cpu_units, steps=1)
         if i >= args.warmup_ref:
@@ -599,9 +601,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    # the reference arm: every "step" is one bounded CPU sample
-    args.steps_ref = max(1, min(args.steps, 2))
-    args.warmup_ref = 0
+    # the reference arm: every "step" is one bounded CPU sample (~0.6 s)
+    args.steps_ref = max(1, args.steps)
+    args.warmup_ref = args.warmup
     if args.impl == "reference":
         run_reference(args)
     elif args.config == "C4":

@@ -226,7 +226,13 @@ class SparseDecoder:
 
     @property
     def kernels_per_step(self) -> int:
-        return 3 if self.scoring == "sketch" else 4
+        """Kernels of one step: sketch stream + select (or score, select,
+        advance) + attention, + the segment merge of the stream attention
+        when an item spans more than one segment."""
+        n = 3 if self.scoring == "sketch" else 4
+        if self.attn_mode == "stream" and self.tiles_hint > max(12, -(-self.tiles_hint // 32)):
+            n += 1
+        return n
 
     # ------------------------------------------------------------------
     def selection(self):

@@ -20,8 +20,13 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "launch__grid_size", "launch__occupancy_limit_registers",
         "launch__occupancy_limit_shared_mem",
         "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"]
-SHORT = {"score_fast_kernel": "decode_score", "score_select_kernel": "score_select",
-         "select_kernel": "decode_select", "attn_mma_kernel": "attn", "advance_kernel": "advance"}
+SHORT = {"score_fast_kernel": "decode_score", "sketch_score_kernel": "sketch_score",
+         "sketch_select_kernel": "select", "select_kernel": "decode_select",
+         "attn_stream_kernel": "attn", "stream_merge_kernel": "attn_merge",
+         "attn_mma_kernel": "attn_split", "advance_kernel": "advance",
+         "prefill_attn_kernel": "prefill_attn", "prefill_plan_kernel": "prefill_plan",
+         "prefill_scores_kernel": "prefill_scores", "split_select_kernel": "split_select",
+         "merge_records_kernel": "split_merge"}
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
@@ -72,7 +77,8 @@ def main():
              f"Launch list `{os.path.basename(lpath)}` (gpu__time_duration.sum; cold-cache and "
              "serialised, so compare shares, not absolutes):", "",
              "| kernel | launches | mean us | share of hot-path time |", "|---|---|---|---|"]
-    hot = {k: v for k, v in L.items() if "dhsa::" in k and "centroids" not in k}
+    once = ("centroids", "sketch_build", "sketch_absmax")  # prefill-time, not per step
+    hot = {k: v for k, v in L.items() if "dhsa::" in k and not any(o in k for o in once)}
     tot = sum(sum(v) / len(v) for v in hot.values())
     for k, v in sorted(hot.items(), key=lambda kv: -sum(kv[1]) / len(kv[1])):
         m = sum(v) / len(v)
