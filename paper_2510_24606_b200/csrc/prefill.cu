@@ -167,16 +167,52 @@ struct PrefillArgs {
 
 template <int MT, int NST>
 struct PrefillSmem {
-  static constexpr int Q = MT * 2 * 16384;         // [mt][D half][128 rows][128 B]
-  static constexpr int KV = 2 * 2 * 8192;           // K [half][64][128B] + V [half][64][128B]
-  static constexpr int P = MT * 16384;             // the P buffer: [mt][128 rows][128 B]
+  static constexpr int Q = MT * 2 * 16384;  // [mt][D half][128 rows][128 B]
+  static constexpr int KV = 2 * 2 * 8192;    // K [half][64][128B] + V [half][64][128B]
   static constexpr int q_off = 0;
   static constexpr int kv_off = Q;
-  static constexpr int p_off = Q + NST * KV;
-  // one P buffer: P_j is written only after PV_{j-1} completed (o_done)
-  static constexpr int total = p_off + P + 1024;  // + alignment slack
+  static constexpr int total = Q + NST * KV + 1024;  // + alignment slack (P lives in TMEM)
 };
 
+// 2^x on the FMA pipe (x <= 8 here): 2^floor(x) * p(frac), p a degree-3
+// minimax polynomial (max rel. error 8.8e-5, far below bf16's 3.9e-3).  Used
+// for half of the softmax exponentials so the MUFU pipe (16/clk/SM) is not
+// the bottleneck (FlashAttention-4's trick).
+__device__ __forceinline__ float exp2_poly(float x) {
+  x = fmaxf(x, -127.f);
+  const float fi = floorf(x);
+  const float f = x - fi;
+  float p = fmaf(f, 0.0790209f, 0.2249411f);
+  p = fmaf(p, f, 0.6960656f);
+  p = fmaf(p, f, 0.9999125f);
+  return __int_as_float(__float_as_int(p) + ((int)fi << 23));
+}
+__device__ __forceinline__ float exp2_mufu(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// D[tmem] (+)= A[tmem] * B[smem] (A = P in TMEM, K-major; "TS" form).
+__device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, {%5, %5, %5, %5}, p;\n\t}" ::"r"(
+          d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(0u)
+      : "memory");
+}
+
+// One CTA = one plan (selection row s, query chunk l) x <= 4 q heads:
+// MT M=128 tiles of 2 heads x 64 rows.  TMEM per tile: two S/P buffers of 64
+// fp32 columns (P is written back as packed bf16 into the first 32 columns
+// of its S buffer and consumed from TMEM by the PV MMA) + O (128 columns).
+// Warp 0: TMA producer; warp 1: MMA issuer; warps 2..: one thread per row.
+// The softmax of block j never waits for PV_{j-1} (the S/P buffers are
+// double-buffered and the tensor pipe executes in issue order) except to
+// rescale O, which happens only when a row max grows by > 2^8.
 template <int MT, int NST>
 __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_kernel(
     const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -187,7 +223,9 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_kernel(
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ __align__(8) uint64_t kv_full[NST], kv_empty[NST], s_full[2], p_full[2], o_done,
+  // o_done[b]: PV of the blocks j with j % 2 == b complete (one phase per
+  // such block; every waiter is then at most one phase behind)
+  __shared__ __align__(8) uint64_t kv_full[NST], kv_empty[NST], s_full[2], p_full[2], o_done[2],
       q_full;
   __shared__ uint32_t s_tmem;
   __shared__ int4 s_plan[288];
@@ -213,8 +251,8 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_kernel(
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 4 * MT);
+      mbar_init(&o_done[i], 1);
     }
-    mbar_init(&o_done, 1);
     mbar_init(&q_full, 1);
     fence_barrier_init();
   }
@@ -225,7 +263,6 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_kernel(
   const uint32_t tmem = s_tmem;
   const uint32_t sq = smem_u32(smem + SM::q_off);
   const uint32_t skv = smem_u32(smem + SM::kv_off);
-  const uint32_t sp = smem_u32(smem + SM::p_off);
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
@@ -270,13 +307,14 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_kernel(
           for (int k = 0; k < D / 16; ++k) {
             const uint64_t ad = umma_sdesc(sq + mt * 32768 + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024);
             const uint64_t bd = umma_sdesc(kb + (k >> 2) * 8192 + (k & 3) * 32, 16, 1024);
-            umma_bf16(tmem + mt * 128 + (j & 1) * 64, ad, bd, idS, k > 0);
+            umma_bf16(tmem + mt * 256 + (j & 1) * 64, ad, bd, idS, k > 0);
           }
         }
         umma_commit(&s_full[j & 1]);
       };
       issue_s(0);
       for (int j = 0; j < np; ++j) {
+        // S_{j+1} overwrites the buffer of P_{j-1}: PV_{j-1} was issued before it
         if (j + 1 < np) issue_s(j + 1);
         mbar_wait(&p_full[j & 1], (j >> 1) & 1);
         tc_fence_after();
@@ -285,14 +323,14 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_kernel(
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {  // 64 keys = 4 x 16
-            const uint64_t ad = umma_sdesc(sp + mt * 16384 + k * 32, 16, 1024);
+          for (int k = 0; k < 4; ++k) {  // 64 keys = 4 x 16; P: 8 packed columns per step
             const uint64_t bd = umma_sdesc(vb + k * 2048, 8192, 1024);
-            umma_bf16(tmem + MT * 128 + mt * 128, ad, bd, idO, (j > 0 || k > 0) ? 1u : 0u);
+            umma_bf16_ts(tmem + mt * 256 + 128, tmem + mt * 256 + (j & 1) * 64 + k * 8, bd, idO,
+                         (j > 0 || k > 0) ? 1u : 0u);
           }
         }
         umma_commit(&kv_empty[st]);
-        umma_commit(&o_done);
+        umma_commit(&o_done[j & 1]);
       }
     }
     __syncwarp();
@@ -310,8 +348,9 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_kernel(
     const int Ri = (int)(keep - 1);
     const int dl = i - bl;
     const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
-    const uint32_t tS = tmem + lane_base + mt * 128;
-    const uint32_t tO = tmem + lane_base + MT * 128 + mt * 128;
+    const uint32_t tS = tmem + lane_base + mt * 256;
+    const uint32_t tO = tS + 128;
+    const float sl2 = a.scale_log2;
     float m_used = -INFINITY, lsum = 0.f;
     for (int j = 0; j < np; ++j) {
       const int4 e = s_plan[j];
@@ -332,17 +371,19 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_kernel(
       tmem_ld32(tS + (j & 1) * 64, *reinterpret_cast<uint32_t(*)[32]>(v));
       tmem_ld32(tS + (j & 1) * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
       tmem_wait_ld();
-      float x[64];
+      // raw max (the scale is positive); masking only where some row needs it
       float mx = -INFINITY;
+      if (__all_sync(0xffffffffu, lim == 64 && self < 0)) {
 #pragma unroll
-      for (int c = 0; c < 64; ++c) {
-        const bool ok = c < lim || c == self;
-        x[c] = ok ? __uint_as_float(v[c]) * a.scale_log2 : -INFINITY;
-        mx = fmaxf(mx, x[c]);
+        for (int c = 0; c < 64; ++c) mx = fmaxf(mx, __uint_as_float(v[c]));
+      } else {
+#pragma unroll
+        for (int c = 0; c < 64; ++c) {
+          if (!(c < lim || c == self)) v[c] = __float_as_uint(-INFINITY);
+          mx = fmaxf(mx, __uint_as_float(v[c]));
+        }
       }
-      // PV of block j-1 done: O is stable and the P buffer is free
-      if (j > 0) mbar_wait(&o_done, (j - 1) & 1);
-      tc_fence_after();
+      mx *= sl2;
       // lazy rescale: a row moves its reference max only when its running max
       // grows by > 2^8 (or on its first finite score, when O holds only
       // zero-weight terms).  TMEM loads/stores are warp-collective, so the
@@ -351,6 +392,10 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_kernel(
       if (mx > -INFINITY && (m_used == -INFINITY || mx > m_used + 8.f)) m_new = mx;
       const bool need = m_used != -INFINITY && m_new != m_used;
       if (__any_sync(0xffffffffu, need)) {
+        // O must hold PV_{j-1} (need implies j >= 1); PV_{j-3} completed
+        // before S_{j-1}, so o_done[(j-1)&1] is at most one phase behind
+        mbar_wait(&o_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+        tc_fence_after();
         const float f = need ? exp2f(m_used - m_new) : 1.f;
 #pragma unroll
         for (int cc = 0; cc < 4; ++cc) {
@@ -366,25 +411,22 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_kernel(
       }
       m_used = m_new;
       const float mref = m_used == -INFINITY ? 0.f : m_used;
-      unsigned char* prow = smem + SM::p_off + mt * 16384 + trow * 128;
+      // p = 2^(s*scale - m): even columns on the MUFU pipe, odd ones on FMA
+      uint32_t pk[32];
 #pragma unroll
-      for (int ch = 0; ch < 8; ++ch) {
-        uint32_t w[4];
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const float p0 = exp2f(x[ch * 8 + 2 * t] - mref);
-          const float p1 = exp2f(x[ch * 8 + 2 * t + 1] - mref);
-          lsum += p0 + p1;
-          w[t] = pack_bf16(p0, p1);
-        }
-        *reinterpret_cast<uint4*>(prow + ((ch ^ (trow & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+      for (int t = 0; t < 32; ++t) {
+        const float p0 = exp2_mufu(fmaf(__uint_as_float(v[2 * t]), sl2, -mref));
+        const float p1 = exp2_poly(fmaf(__uint_as_float(v[2 * t + 1]), sl2, -mref));
+        lsum += p0 + p1;
+        pk[t] = pack_bf16(p0, p1);
       }
-      fence_proxy_async_smem();
+      tmem_st32(tS + (j & 1) * 64, pk);  // P over the first 32 columns of its S buffer
+      tmem_wait_st();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[j & 1]);
     }
-    mbar_wait(&o_done, (np - 1) & 1);
+    mbar_wait(&o_done[(np - 1) & 1], ((np - 1) >> 1) & 1);  // in-order: every PV done
     tc_fence_after();
     const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
     __nv_bfloat16* orow = a.out + ((int64_t)(qh0 + (rg < nh ? rg : 0)) * a.L + i) * D;
@@ -396,12 +438,12 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_kernel(
       if (live) {
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
-          uint4 pk;
-          pk.x = pack_bf16(__uint_as_float(o[8 * t + 0]) * inv, __uint_as_float(o[8 * t + 1]) * inv);
-          pk.y = pack_bf16(__uint_as_float(o[8 * t + 2]) * inv, __uint_as_float(o[8 * t + 3]) * inv);
-          pk.z = pack_bf16(__uint_as_float(o[8 * t + 4]) * inv, __uint_as_float(o[8 * t + 5]) * inv);
-          pk.w = pack_bf16(__uint_as_float(o[8 * t + 6]) * inv, __uint_as_float(o[8 * t + 7]) * inv);
-          *reinterpret_cast<uint4*>(orow + cc * 32 + 8 * t) = pk;
+          uint4 pk4;
+          pk4.x = pack_bf16(__uint_as_float(o[8 * t + 0]) * inv, __uint_as_float(o[8 * t + 1]) * inv);
+          pk4.y = pack_bf16(__uint_as_float(o[8 * t + 2]) * inv, __uint_as_float(o[8 * t + 3]) * inv);
+          pk4.z = pack_bf16(__uint_as_float(o[8 * t + 4]) * inv, __uint_as_float(o[8 * t + 5]) * inv);
+          pk4.w = pack_bf16(__uint_as_float(o[8 * t + 6]) * inv, __uint_as_float(o[8 * t + 7]) * inv);
+          *reinterpret_cast<uint4*>(orow + cc * 32 + 8 * t) = pk4;
         }
       }
     }
@@ -519,6 +561,6 @@ extern "C" int dhsa_prefill_attn(const void* q, const void* k, const void* v, in
   a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)D));
   const int S = per_head ? U * G : U;
   cudaStream_t st = (cudaStream_t)stream;
-  if (a.heads_per_cta > 2) return launch_prefill_attn<2, 3>(mq, mk, mv, a, S, st);
+  if (a.heads_per_cta > 2) return launch_prefill_attn<2, 4>(mq, mk, mv, a, S, st);
   return launch_prefill_attn<1, 5>(mq, mk, mv, a, S, st);
 }
