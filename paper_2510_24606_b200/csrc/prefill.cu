@@ -42,40 +42,71 @@ namespace dhsa {
 // ------------------------------------------------------------------- K7 --
 // S[s][l][c] = agg_{j in heads(s)} Qc[q(s,j)][l] . Kc[u(s)][c] for c <= l, fp64
 // (dot products accumulated in dimension order, aggregated max / mean).
+// 64 x 64 output tiles (lower triangle only), 256 threads x 4 x 4 register
+// tile, D streamed through shared memory in slabs of 16; the K tile is
+// loaded once per slab for all G heads of the selection row.
+constexpr int kScT = 64, kScSlab = 16;
+
 __global__ __launch_bounds__(256) void prefill_scores_kernel(
     const double* __restrict__ qc, const double* __restrict__ kc, int nc, int D, int G,
     int per_head, int agg, double* __restrict__ out) {
-  __shared__ double a[16][33];
-  __shared__ double b[16][33];
+  __shared__ double sq[kScSlab][kScT + 1];
+  __shared__ double sk[kScSlab][kScT + 1];
   const int s = blockIdx.z;
-  const int i0 = blockIdx.y * 16, j0 = blockIdx.x * 16;
-  if (j0 > i0 + 15) return;  // strictly above the diagonal: never read
-  const int ty = threadIdx.x / 16, tx = threadIdx.x % 16;
+  const int i0 = blockIdx.y * kScT, j0 = blockIdx.x * kScT;
+  if (j0 > i0) return;  // strictly above the diagonal: never read
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // 16 x 16 threads, 4 x 4 each
   const int u = per_head ? s / G : s;
   const int nh = per_head ? 1 : G;
   const int h0 = per_head ? s : s * G;
   const double* K = kc + (int64_t)u * nc * D;
-  double res = 0.0;
+  double res[4][4];
   for (int j = 0; j < nh; ++j) {
     const double* Q = qc + (int64_t)(h0 + j) * nc * D;
-    double acc = 0.0;
-    for (int d0 = 0; d0 < D; d0 += 32) {
-      for (int e = threadIdx.x; e < 16 * 32; e += 256) {
-        const int r = e / 32, c = e % 32;
-        a[r][c] = (i0 + r < nc && d0 + c < D) ? Q[(int64_t)(i0 + r) * D + d0 + c] : 0.0;
-        b[r][c] = (j0 + r < nc && d0 + c < D) ? K[(int64_t)(j0 + r) * D + d0 + c] : 0.0;
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    for (int d0 = 0; d0 < D; d0 += kScSlab) {
+      for (int e = threadIdx.x; e < kScT * kScSlab; e += 256) {
+        const int r = e / kScSlab, c = e % kScSlab;
+        sq[c][r] = (i0 + r < nc && d0 + c < D) ? Q[(int64_t)(i0 + r) * D + d0 + c] : 0.0;
+        sk[c][r] = (j0 + r < nc && d0 + c < D) ? K[(int64_t)(j0 + r) * D + d0 + c] : 0.0;
       }
       __syncthreads();
-#pragma unroll 8
-      for (int c = 0; c < 32; ++c) acc = fma(a[ty][c], b[tx][c], acc);
+#pragma unroll
+      for (int c = 0; c < kScSlab; ++c) {
+        double qa[4], kb[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) qa[a] = sq[c][ty + 16 * a];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) kb[b] = sk[c][tx + 16 * b];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[a][b] = fma(qa[a], kb[b], acc[a][b]);
+      }
       __syncthreads();
     }
-    if (j == 0) res = acc;
-    else if (agg == DHSA_AGG_MAX) res = fmax(res, acc);
-    else res = res + acc;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        if (j == 0) res[a][b] = acc[a][b];
+        else if (agg == DHSA_AGG_MAX) res[a][b] = fmax(res[a][b], acc[a][b]);
+        else res[a][b] = res[a][b] + acc[a][b];
+      }
   }
-  if (agg == DHSA_AGG_MEAN && nh > 1) res = res / (double)nh;
-  if (i0 + ty < nc && j0 + tx < nc) out[((int64_t)s * nc + i0 + ty) * nc + j0 + tx] = res;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      double v = res[a][b];
+      if (agg == DHSA_AGG_MEAN && nh > 1) v = v / (double)nh;
+      const int ri = i0 + ty + 16 * a, cj = j0 + tx + 16 * b;
+      if (ri < nc && cj < nc) out[((int64_t)s * nc + ri) * nc + cj] = v;
+    }
 }
 
 // ------------------------------------------------------------------- K8 --
@@ -473,7 +504,7 @@ extern "C" int dhsa_prefill_scores(const double* q_centroids, const double* k_ce
                "dhsa_prefill_scores: unknown aggregation %d", agg);
   const int per_head = agg == DHSA_AGG_NONE;
   const int S = per_head ? U * G : U;
-  const int t = (n_chunks + 15) / 16;
+  const int t = (n_chunks + kScT - 1) / kScT;
   dim3 grid((unsigned)t, (unsigned)t, (unsigned)S);
   prefill_scores_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(q_centroids, k_centroids, n_chunks,
                                                                  D, G, per_head, agg, scores);
