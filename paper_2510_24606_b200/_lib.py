@@ -12,7 +12,7 @@ import os
 import re
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdhsa_b200.so")
+LIB_PATH = os.environ.get("DHSA_LIB_PATH") or os.path.join(_HERE, "libdhsa_b200.so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "dhsa_b200.h")
 
 F64, F32, BF16 = 0, 1, 2

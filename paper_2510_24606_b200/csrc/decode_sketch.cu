@@ -39,9 +39,13 @@
 #include <cuda_fp16.h>
 #include <cstdlib>
 
+#ifndef SELECT_THREADS
+#define SELECT_THREADS 256
+#endif
+
 namespace dhsa {
 
-constexpr int kSelectThreads = 512;
+constexpr int kSelectThreads = SELECT_THREADS;
 constexpr int kSmallUncertain = 1024;
 
 constexpr int ilog2c(int x) { return x <= 1 ? 0 : 1 + ilog2c(x / 2); }
@@ -497,16 +501,19 @@ __global__ __launch_bounds__(kSelectThreads) void sketch_select_kernel(SketchArg
   const int g = a.gen_count[u];
   const int gl = (a.split && !a.owns_tail) ? 0 : g;  // generated tokens held by this shard
   constexpr int DV = D / 32;
-  if (warp < G) {
-    double t = 0.0;
+  static_assert(NW >= 2, "select needs >= 2 warps");
+  if (warp < NW - 1) {  // query norms (certified bound), warps 0 .. NW-2
+    for (int h = warp; h < G; h += NW - 1) {
+      double t = 0.0;
 #pragma unroll
-    for (int v = 0; v < DV; ++v) {
-      const double x = to_f64(a.q[(int64_t)(u * G + warp) * D + lane + 32 * v]);
-      t = fma(x, x, t);
+      for (int v = 0; v < DV; ++v) {
+        const double x = to_f64(a.q[(int64_t)(u * G + h) * D + lane + 32 * v]);
+        t = fma(x, x, t);
+      }
+      t = warp_sum(t);
+      if (lane == 0) s_qn[h] = sqrt(t) * (1.0 + 1e-12);
     }
-    t = warp_sum(t);
-    if (lane == 0) s_qn[warp] = sqrt(t) * (1.0 + 1e-12);
-  } else if (warp == NW - 1) {
+  } else {
     // generated chunk, exact fp64 (masks.py:161), then the state update
     double* gs = a.gen_sum + (int64_t)u * D;
     double gv[DV], qv[G][DV];
