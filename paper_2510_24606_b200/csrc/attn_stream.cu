@@ -25,6 +25,7 @@ namespace dhsa {
 
 constexpr int kStreamMaxSeg = 32;  // record slots per item (bounds the workspace)
 constexpr int kSegTiles = 12;      // tiles per segment (at least)
+constexpr int kSegSmall = 4;       // ... in the tail of the step
 
 struct StreamArgs {
   const __nv_bfloat16* q;
@@ -33,8 +34,12 @@ struct StreamArgs {
   const int32_t* tiles;
   int64_t tile_cap;
   const int32_t* ntiles;
-  int seg_tiles;      // S: tiles per segment
-  int nseg;           // virtual segments per item: ceil(tiles_hint / S) <= kStreamMaxSeg
+  // Segments: the first head_items items use seg_big tiles per segment, the
+  // last ones seg_small, so the final pulls of the step are short and the
+  // per-CTA speed spread leaves a short tail.  nseg_* = ceil(tiles_hint / seg_*)
+  // <= kStreamMaxSeg virtual segments per item.
+  int seg_big, nseg_big, seg_small, nseg_small, head_items;
+  int prefetch;       // fetch the next pull while the current one streams
   __nv_bfloat16* out;
   float* rec_out;     // unnormalised records instead of out (split-KV shards)
   float* ws;          // [items][kStreamMaxSeg][GH][D+2]
@@ -54,6 +59,11 @@ struct RingMeta {
 
 
 // tiles [lo, hi) of virtual segment j of an item with nt real tiles
+__device__ __forceinline__ void seg_shape(const StreamArgs& a, int item, int& S, int& nseg) {
+  const bool head = item < a.head_items;
+  S = head ? a.seg_big : a.seg_small;
+  nseg = head ? a.nseg_big : a.nseg_small;
+}
 __device__ __forceinline__ void seg_range(int j, int S, int nseg, int nt, int& lo, int& hi) {
   lo = min(j * S, nt);
   hi = (j == nseg - 1) ? nt : min((j + 1) * S, nt);
@@ -116,7 +126,8 @@ __global__ __launch_bounds__(192, 2) void attn_stream_kernel(const __grid_consta
       prefetch_tmap(&tmK);
       prefetch_tmap(&tmV);
     }
-    const int total = a.items * a.nseg;
+    const int head_pulls = a.head_items * a.nseg_big;
+    const int total = head_pulls + (a.items - a.head_items) * a.nseg_small;
     int it = 0;
     auto slot = [&]() {
       const int st = it % STAGES;
@@ -128,8 +139,19 @@ __global__ __launch_bounds__(192, 2) void attn_stream_kernel(const __grid_consta
     for (;;) {
       const int k = __shfl_sync(0xffffffffu, knext, 0);
       if (k >= total) break;
-      if (lane == 0) knext = atomicAdd(pull, 1);  // the next pull, in flight meanwhile
-      const int item = k / a.nseg, j = k - item * a.nseg;
+      // the next pull is fetched while this one streams (a.prefetch), or
+      // only once this one has been queued
+      if (lane == 0 && a.prefetch) knext = atomicAdd(pull, 1);
+      int item, j;
+      if (k < head_pulls) {
+        item = k / a.nseg_big;
+        j = k - item * a.nseg_big;
+      } else {
+        item = a.head_items + (k - head_pulls) / a.nseg_small;
+        j = k - head_pulls - (item - a.head_items) * a.nseg_small;
+      }
+      int S, nseg;
+      seg_shape(a, item, S, nseg);
       int nt = 0;
       if (lane == 0) {
         if (a.ready) spin_geq(a.ready + item, 1);
@@ -137,8 +159,11 @@ __global__ __launch_bounds__(192, 2) void attn_stream_kernel(const __grid_consta
       }
       nt = __shfl_sync(0xffffffffu, nt, 0);
       int lo, hi;
-      seg_range(j, a.seg_tiles, a.nseg, nt, lo, hi);
-      if (lo >= hi && !(nt == 0 && j == 0)) continue;  // beyond the item's real tiles
+      seg_range(j, S, nseg, nt, lo, hi);
+      if (lo >= hi && !(nt == 0 && j == 0)) {  // beyond the item's real tiles
+        if (lane == 0 && !a.prefetch) knext = atomicAdd(pull, 1);
+        continue;
+      }
       const int32_t* tl = a.tiles + (int64_t)item * a.tile_cap * 2;
       const int64_t row0 = (int64_t)(item / a.items_per_unit) * a.cache_rows;
       for (int t0 = lo; t0 < hi; t0 += 32) {
@@ -167,6 +192,7 @@ __global__ __launch_bounds__(192, 2) void attn_stream_kernel(const __grid_consta
         const int st = slot();
         meta[st] = RingMeta{kEnd, item, j, hi - lo, nt};
         mbar_arrive(&full_bar[st]);
+        if (!a.prefetch) knext = atomicAdd(pull, 1);
       }
       ++it;
     }
@@ -272,10 +298,13 @@ template <int D>
 __global__ __launch_bounds__(D) void stream_merge_kernel(StreamArgs a) {
   constexpr int REC = D + 2;
   pdl_wait();
+  if (a.dbg && threadIdx.x == 0) atomicMin(a.dbg + kDbgAttn + 8192, gtimer());
   const int item = blockIdx.x, h = blockIdx.y, d = threadIdx.x, GH = a.GH;
   const int nt = __ldcg(a.ntiles + item);
   int lo, hi;
-  seg_range(0, a.seg_tiles, a.nseg, nt, lo, hi);
+  int S, nseg;
+  seg_shape(a, item, S, nseg);
+  seg_range(0, S, nseg, nt, lo, hi);
   if (hi - lo == nt) return;  // one segment: written directly by the attention
   const float* slots = a.ws + (int64_t)item * kStreamMaxSeg * GH * REC + h * REC;
   float mv[kStreamMaxSeg], lv[kStreamMaxSeg], av[kStreamMaxSeg];
@@ -283,8 +312,8 @@ __global__ __launch_bounds__(D) void stream_merge_kernel(StreamArgs a) {
   for (int sg = 0; sg < kStreamMaxSeg; ++sg) {  // independent loads, issued together
     mv[sg] = -INFINITY;
     lv[sg] = av[sg] = 0.f;
-    if (sg < a.nseg) {
-      seg_range(sg, a.seg_tiles, a.nseg, nt, lo, hi);
+    if (sg < nseg) {
+      seg_range(sg, S, nseg, nt, lo, hi);
       if (lo < hi) {
         const float* r = slots + sg * GH * REC;
         mv[sg] = __ldcg(r);
@@ -306,6 +335,7 @@ __global__ __launch_bounds__(D) void stream_merge_kernel(StreamArgs a) {
   }
   store_row<D>(a, item, h, d, mstar, lsum, acc,
                a.rec_out ? a.rec_out + ((int64_t)item * GH + h) * REC : nullptr);
+  if (a.dbg && threadIdx.x == 0) atomicMax(a.dbg + kDbgAttn + 8193, gtimer());
 }
 
 template <int D, int STAGES>
@@ -324,7 +354,14 @@ static int launch_stream(const CUtensorMap& mk, const CUtensorMap& mv, StreamArg
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 192, smem);
   int64_t C = (int64_t)sms * (per_sm < 1 ? 1 : per_sm);
-  const int64_t pulls = (int64_t)a.items * a.nseg;
+  // the last ~2 pulls per CTA use small segments
+  a.head_items = a.items;
+  if (a.nseg_small > a.nseg_big) {
+    const int64_t tail = (2 * C + a.nseg_small - 1) / a.nseg_small;
+    a.head_items = (int)(a.items > tail ? a.items - tail : 0);
+  }
+  const int64_t pulls = (int64_t)a.head_items * a.nseg_big +
+                        (int64_t)(a.items - a.head_items) * a.nseg_small;
   if (C > pulls) C = pulls;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)C);
@@ -341,7 +378,8 @@ static int launch_stream(const CUtensorMap& mk, const CUtensorMap& mv, StreamArg
     set_error("dhsa_attn_stream: %s", cudaGetErrorString(e));
     return DHSA_ECUDA;
   }
-  if (a.nseg > 1) {  // cross-segment merge, launched early (programmatic dependency)
+  if (a.nseg_big > 1 || (a.head_items < a.items && a.nseg_small > 1)) {
+    // cross-segment merge, launched early (programmatic dependency)
     cudaLaunchConfig_t mc{};
     mc.gridDim = dim3((unsigned)a.items, (unsigned)a.GH);
     mc.blockDim = dim3(D);
@@ -407,8 +445,12 @@ extern "C" int dhsa_attn_stream(const void* q, const void* k_cache, const void* 
   a.ntiles = ntiles;
   int seg = kSegTiles;
   if (const char* e = getenv("DHSA_SEG_TILES")) seg = atoi(e) > 0 ? atoi(e) : seg;
-  a.seg_tiles = max(seg, (tiles_hint + kStreamMaxSeg - 1) / kStreamMaxSeg);
-  a.nseg = (tiles_hint + a.seg_tiles - 1) / a.seg_tiles;
+  a.prefetch = 0;  // measured: prefetching the next pull lengthens the tail
+  if (const char* e = getenv("DHSA_STREAM_PREFETCH")) a.prefetch = atoi(e);
+  a.seg_big = max(seg, (tiles_hint + kStreamMaxSeg - 1) / kStreamMaxSeg);
+  a.nseg_big = (tiles_hint + a.seg_big - 1) / a.seg_big;
+  a.seg_small = max(kSegSmall, (tiles_hint + kStreamMaxSeg - 1) / kStreamMaxSeg);
+  a.nseg_small = (tiles_hint + a.seg_small - 1) / a.seg_small;
   a.out = (__nv_bfloat16*)out;
   a.rec_out = records;
   a.ws = (float*)workspace;

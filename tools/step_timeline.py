@@ -37,6 +37,7 @@ for _ in range(5):
     gr.replay()
 torch.cuda.synchronize()
 dbg.zero_()
+dbg[131072 + 8192] = 2 ** 62  # merge kernel: min start / max end
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
 gr.replay()
@@ -48,10 +49,8 @@ sk = sk[sk[:, 0] > 0]
 t0 = sk[:, 0].min()
 sel = t[:dec.U * 16].reshape(dec.U, 16)
 at = t[131072:131072 + 4 * 2048].reshape(-1, 4)
-ep = t[131072 + 8192:131072 + 8192 + 4 * 2048].reshape(-1, 4)
 live = at[:, 0] > 0
 at = at[live]
-ep = ep[live]
 
 
 def show(name, col):
@@ -70,6 +69,9 @@ for k_, n in [(0, "select start"), (1, "select after pdl_wait"), (3, "select aft
 show("attn CTA start", at[:, 0])
 show("attn first tile", at[:, 1])
 show("attn CTA end", at[:, 2])
+mg = t[131072 + 8192:131072 + 8194]
+if mg[1] > 0:
+    print(f"merge kernel: first start {(mg[0] - t0) / 1e3:.2f} us, last end {(mg[1] - t0) / 1e3:.2f} us")
 print("uncertain chunks per unit: median", np.median(sel[:, 15]), "max", sel[:, 15].max())
 ends = (at[:, 2] - t0) / 1e3
 ntl = at[:, 3] & 0xFFFFFFFF
