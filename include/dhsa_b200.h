@@ -206,7 +206,12 @@ int64_t dhsa_sketch_select_scratch_size(int max_chunks);
  * prologue (query staging, generated-chunk update) overlaps the sketch stream
  * and it waits (griddepcontrol.wait) before reading the scores.
  * ready: int32[items] (or NULL) flags raised when an item's tiles are final,
- * consumed by dhsa_attn(..., ready, ...). */
+ * consumed by dhsa_attn / dhsa_attn_stream (re-armed by the next step's
+ * sketch stream).
+ * progress: int32[U] zero at rest, or NULL: per-unit slice counters from the
+ * sketch stream to the select, so a unit is selected as soon as its own
+ * centroids are scored (re-armed in-kernel); NULL waits for the whole
+ * stream. */
 int dhsa_decode_step_bf16(const void* q, const void* sketch, int64_t sk_unit_stride,
                           const float* sinfo, const double* centroids,
                           int64_t c_unit_stride, double* gen_sum, int32_t* gen_count,
@@ -215,7 +220,7 @@ int dhsa_decode_step_bf16(const void* q, const void* sketch, int64_t sk_unit_str
                           int U, int G, int D, int agg, int64_t budget, int tile_tokens,
                           int32_t* tiles, int64_t tile_cap, int32_t* ntiles, float* approx,
                           int64_t sc_stride, void* scratch, int32_t* ready, int advance,
-                          dhsa_stream_t stream);
+                          int32_t* progress, dhsa_stream_t stream);
 
 /* ---- sequence-sharded split-KV decode (1M-token contexts over GPUs) --------
  * A sequence is cut into W contiguous shards (one per GPU); shard r holds
@@ -261,7 +266,7 @@ int dhsa_decode_candidates_bf16(const void* q, const void* sketch, int64_t sk_un
                                 int U, int G, int D, int agg, int64_t budget,
                                 dhsa_split_shard shard, void* cand, int64_t cand_stride,
                                 int cand_cap, float* approx, int64_t sc_stride, void* scratch,
-                                dhsa_stream_t stream);
+                                int32_t* progress, dhsa_stream_t stream);
 
 /* Step 3: the global walk (masks.topk_row order: score desc, chunk asc) over
  * the W gathered candidate rows of every item (gathered + r * rank_stride

@@ -63,11 +63,11 @@ _SIGS = {
     "dhsa_decode_step_bf16": (C.c_int, [vp, vp, C.c_int64, vp, vp, C.c_int64, vp, vp, vp, vp,
                                         vp, vp, C.c_int64, Layout, C.c_int, C.c_int, C.c_int,
                                         C.c_int, C.c_int64, C.c_int, vp, C.c_int64, vp, vp,
-                                        C.c_int64, vp, vp, C.c_int, vp]),
+                                        C.c_int64, vp, vp, C.c_int, vp, vp]),
     "dhsa_decode_candidates_bf16": (C.c_int, [vp, vp, C.c_int64, vp, vp, C.c_int64, vp, vp, vp,
                                               vp, vp, vp, C.c_int64, Layout, C.c_int, C.c_int,
                                               C.c_int, C.c_int, C.c_int64, ShardSpec, vp,
-                                              C.c_int64, C.c_int, vp, C.c_int64, vp, vp]),
+                                              C.c_int64, C.c_int, vp, C.c_int64, vp, vp, vp]),
     "dhsa_split_select": (C.c_int, [vp, C.c_int, C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int,
                                     vp, vp, C.c_int, C.c_int64, C.c_int, C.c_int, C.c_int, vp,
                                     C.c_int64, vp, C.c_int, vp]),

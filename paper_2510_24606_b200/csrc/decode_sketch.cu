@@ -81,6 +81,7 @@ struct SketchArgs {
   int advance;
   int32_t* ready;           // [items] select -> attention flags (zeroed by the sketch kernel) or null
   int n_units;
+  int32_t* progress;        // [U] sketch -> select: consumer-warp slices done (zero at rest) or null
   unsigned long long* dbg;  // optional per-CTA phase timestamps (DHSA_DEBUG_TIMING)
   // sequence-sharded split-KV mode (dhsa_decode_candidates_bf16): this shard
   // holds global prompt chunks [chunk_offset, chunk_offset + nchunks); the
@@ -212,6 +213,17 @@ __global__ __launch_bounds__(kTcThreads) void sketch_score_kernel(
   }
 
   // ---------------- consumers ----------------
+  // progress: one release per (warp, unit) run of slices, not per slice (a
+  // fence per slice measurably slows the stream)
+  int pend_u = -1, pend_n = 0;
+  auto publish = [&](int pu, int pn) {
+    if (!a.progress || pu < 0 || pn == 0) return;
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence();
+      atomicAdd(a.progress + pu, pn);
+    }
+  };
   const int hcol = lane >> 2;  // B column (head) owned for the fragment
   uint32_t qb[KS][2];
   int kq0 = 0, kq1 = 0;        // scale exponents of the two heads in this lane's C columns
@@ -227,6 +239,9 @@ __global__ __launch_bounds__(kTcThreads) void sketch_score_kernel(
     }
     if (c0 >= nc) continue;
     if (u != cur_u) {
+      publish(pend_u, pend_n);
+      pend_u = u;
+      pend_n = 0;
       cur_u = u;
       // B fragments of q'^T: head hcol, dims 16ks + 2(lane&3) + {0,1} (+8)
       float qv[KS][4];
@@ -306,7 +321,9 @@ __global__ __launch_bounds__(kTcThreads) void sketch_score_kernel(
         if (c0 + r0 + 8 < nc) a.approx[(int64_t)u * a.sc_stride + c0 + r0 + 8] = y;
       }
     }
+    ++pend_n;  // slices of unit pend_u this warp has scored, published per unit
   }
+  publish(pend_u, pend_n);
   if (a.dbg && threadIdx.x == 0) a.dbg[kDbgSketch + 2 * blockIdx.x + 1] = gtimer();
 }
 
@@ -555,8 +572,18 @@ __global__ __launch_bounds__(kSelectThreads) void sketch_select_kernel(SketchArg
       }
     }
   }
-  // the approximate scores are complete once the score grid has finished
-  pdl_wait();
+  // the unit's approximate scores are complete once every consumer warp of
+  // every slice of the unit has published (progress), or - without progress
+  // counters - once the whole score grid has finished
+  if (a.progress) {
+    if (tid == 0) {
+      const int slices = (a.lay.num_chunks(u) + kSliceRows - 1) / kSliceRows;
+      spin_geq(a.progress + u, kTcConsumers * slices);
+      a.progress[u] = 0;  // re-arm: the next step's stream starts after this grid
+    }
+  } else {
+    pdl_wait();
+  }
   __syncthreads();
   DBG_T(1);
 
@@ -893,7 +920,7 @@ static int decode_step_impl(
     const void* k_new, const void* v_new, void* k_cache, void* v_cache, int64_t cache_unit_stride,
     dhsa_layout layout, int U, int G, int D, int agg, int64_t budget, int tile_tokens,
     int32_t* tiles, int64_t tile_cap, int32_t* ntiles, float* approx, int64_t sc_stride,
-    void* scratch, int32_t* ready, int advance, dhsa_stream_t stream,
+    void* scratch, int32_t* ready, int advance, int32_t* progress, dhsa_stream_t stream,
     const dhsa_split_shard* shard = nullptr, void* cand = nullptr, int64_t cand_stride = 0,
     int cand_cap = 0) {
   DHSA_REQUIRE(q && sketch && sinfo && centroids && gen_sum && gen_count &&
@@ -936,6 +963,7 @@ static int decode_step_impl(
   a.advance = advance;
   a.ready = ready;
   a.n_units = U;
+  a.progress = progress;
   if (shard) {
     DHSA_REQUIRE(cand && cand_cap >= 1 && cand_stride >= (int64_t)sizeof(SplitCand) * (cand_cap + 1) &&
                      cand_stride % 8 == 0,
@@ -978,11 +1006,11 @@ extern "C" int dhsa_decode_step_bf16(
     const void* k_new, const void* v_new, void* k_cache, void* v_cache, int64_t cache_unit_stride,
     dhsa_layout layout, int U, int G, int D, int agg, int64_t budget, int tile_tokens,
     int32_t* tiles, int64_t tile_cap, int32_t* ntiles, float* approx, int64_t sc_stride,
-    void* scratch, int32_t* ready, int advance, dhsa_stream_t stream) {
+    void* scratch, int32_t* ready, int advance, int32_t* progress, dhsa_stream_t stream) {
   return decode_step_impl(q, sketch, sk_unit_stride, sinfo, centroids, c_unit_stride, gen_sum,
                           gen_count, k_new, v_new, k_cache, v_cache, cache_unit_stride, layout, U,
                           G, D, agg, budget, tile_tokens, tiles, tile_cap, ntiles, approx,
-                          sc_stride, scratch, ready, advance, stream);
+                          sc_stride, scratch, ready, advance, progress, stream);
 }
 
 extern "C" int dhsa_decode_candidates_bf16(
@@ -991,10 +1019,10 @@ extern "C" int dhsa_decode_candidates_bf16(
     const void* k_new, const void* v_new, void* k_cache, void* v_cache, int64_t cache_unit_stride,
     dhsa_layout layout, int U, int G, int D, int agg, int64_t budget, dhsa_split_shard shard,
     void* cand, int64_t cand_stride, int cand_cap, float* approx, int64_t sc_stride,
-    void* scratch, dhsa_stream_t stream) {
+    void* scratch, int32_t* progress, dhsa_stream_t stream) {
   return decode_step_impl(q, sketch, sk_unit_stride, sinfo, centroids, c_unit_stride, gen_sum,
                           const_cast<int32_t*>(gen_count), k_new, v_new, k_cache, v_cache,
                           cache_unit_stride, layout, U, G, D, agg, budget, 64, nullptr, 2, nullptr,
-                          approx, sc_stride, scratch, nullptr, 0, stream, &shard, cand,
+                          approx, sc_stride, scratch, nullptr, 0, progress, stream, &shard, cand,
                           cand_stride, cand_cap);
 }

@@ -120,6 +120,7 @@ class SparseDecoder:
             self.sinfo = torch.zeros(self.U, 4, dtype=torch.float32, **kw)
             self.approx = torch.empty(self.items, self.nc_cap + 1, dtype=torch.float32, **kw)
             self.ready = torch.zeros(self.items, dtype=torch.int32, **kw)
+            self.progress = torch.zeros(self.U, dtype=torch.int32, **kw)
             per_unit = _lib.load().dhsa_sketch_select_scratch_size(self.nc_cap)
             self.scratch = (torch.empty(self.U * per_unit, dtype=torch.uint8, **kw)
                             if per_unit > 0 else None)
@@ -184,7 +185,7 @@ class SparseDecoder:
                           self.D, agg, self.budget, self.tile, _lib.ptr(self.tiles),
                           self.tile_cap, _lib.ptr(self.ntiles), _lib.ptr(self.approx),
                           self.nc_cap + 1, _lib.ptr(self.scratch), _lib.ptr(self.ready), 1,
-                          st)
+                          _lib.ptr(self.progress), st)
             return [("score_select", fused), attn]
 
         def score():
