@@ -9,7 +9,7 @@ There is no CPU fallback: GPU entry points raise if the library or the
 device is missing.
 """
 
-from .chunking import check_boundaries, extend_for_decode, static_boundaries
+from .chunking import check_boundaries, extend_for_decode, nms_boundaries, static_boundaries
 from .core import TokenSequence, dense_attention
 from .chunk_repr import ChunkReps, aggregate_chunk, aggregate_rows, build_chunk_reps, \
     chunk_similarity
@@ -20,7 +20,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "TokenSequence", "dense_attention",
-    "check_boundaries", "static_boundaries", "extend_for_decode",
+    "check_boundaries", "static_boundaries", "nms_boundaries", "extend_for_decode",
     "ChunkReps", "aggregate_chunk", "aggregate_rows", "build_chunk_reps", "chunk_similarity",
     "CostCounters", "SparsityMask", "upsample", "topk_row", "mask_from_chunk_scores",
     "prefill_mask", "decode_mask_row", "DecodeSession",

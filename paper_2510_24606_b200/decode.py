@@ -51,7 +51,7 @@ class SparseDecoder:
 
     def __init__(self, batch, q_heads, kv_heads, head_dim, max_len, *, block=64, top_k=64,
                  budget=None, dtype=torch.bfloat16, agg="max", tile=64, splits=None,
-                 device=None, scoring=None, attn_mode=None):
+                 device=None, scoring=None, attn_mode=None, max_chunks=None):
         _lib.require_cuda()
         if q_heads % kv_heads:
             raise ValueError("q_heads must be a multiple of kv_heads")
@@ -73,7 +73,9 @@ class SparseDecoder:
         self.tile = int(tile)
         self.dev = torch.device(device) if device is not None else torch.device("cuda")
         self.L_cap = ((int(max_len) + 64 - 1) // 64) * 64 + 64
-        self.nc_cap = (int(max_len) + self.block - 1) // self.block
+        # chunk capacity per unit: the static grid's count, or more for
+        # dynamic (e.g. NMS) boundaries with short chunks
+        self.nc_cap = int(max_chunks) if max_chunks else (int(max_len) + self.block - 1) // self.block
         kw = dict(device=self.dev)
         self.k_cache = torch.zeros(batch, kv_heads, self.L_cap, head_dim, dtype=dtype, **kw)
         self.v_cache = torch.zeros_like(self.k_cache)
@@ -107,6 +109,8 @@ class SparseDecoder:
         self.counters = torch.zeros(ncnt, dtype=torch.int32, **kw)
         self.max_prompt = 0
         self.max_chunks = 0
+        self.bounds = self.nchunks = None
+        self.chunk_counts = [0] * self.U
         self.steps = 0
         # scoring: "sketch" (fp16 centroid sketch + certified fp64 re-scoring at
         # the cut; sketch stream + select kernels) or "fp64" (stream fp64 centroids)
@@ -127,21 +131,51 @@ class SparseDecoder:
 
     # ------------------------------------------------------------------
     def _layout(self):
+        if self.bounds is not None:  # explicit per-unit boundaries (chunking.py:23-39)
+            return _lib.layout(bounds=self.bounds, bounds_stride=self.nc_cap + 1,
+                               nchunks=self.nchunks, plen=self.plen, max_chunks=self.max_chunks)
         return _lib.layout(plen=self.plen, block=self.block, max_chunks=self.max_chunks)
 
-    def prefill(self, keys, values, prompt_len=None):
+    def _set_bounds(self, bounds, P):
+        """bounds: None (static grid of `block`), one boundary list shared by
+        every unit, or one list per unit (B*Hkv lists, unit = b*Hkv + h) —
+        the reference's `bounds` ([0, ..., P], strictly increasing; validated
+        like chunking.check_boundaries)."""
+        self.bounds = self.nchunks = None
+        self.chunk_counts = [(P + self.block - 1) // self.block] * self.U
+        if bounds is None:
+            return
+        from .chunking import check_boundaries
+
+        lists = [bounds] * self.U if bounds and not hasattr(bounds[0], "__len__") else list(bounds)
+        if len(lists) != self.U:
+            raise ValueError(f"expected one boundary list per unit ({self.U}), got {len(lists)}")
+        rows = []
+        for b in lists:
+            b = check_boundaries([int(x) for x in b], P)
+            if len(b) - 1 > self.nc_cap:
+                raise ValueError(f"{len(b) - 1} chunks exceed max_chunks={self.nc_cap}")
+            rows.append(b + [P] * (self.nc_cap + 1 - len(b)))
+        self.chunk_counts = [len(b) - 1 for b in lists]
+        self.bounds = torch.tensor(rows, dtype=torch.int32, device=self.dev)
+        self.nchunks = torch.tensor(self.chunk_counts, dtype=torch.int32, device=self.dev)
+
+    def prefill(self, keys, values, prompt_len=None, bounds=None):
         """Load prompt K/V [B, Hkv, P, D] into the cache and build the fp64
-        centroid cache (K1, chunk_repr.aggregate_rows semantics)."""
+        centroid cache (K1, chunk_repr.aggregate_rows semantics).  ``bounds``
+        gives dynamic chunk boundaries (see ``_set_bounds``); default is the
+        static grid of ``block`` tokens (chunking.static_boundaries)."""
         P = keys.shape[2] if prompt_len is None else int(prompt_len)
         if P < 1 or P + 1 > self.L_cap - 64:
             raise ValueError("prompt does not fit the cache")
+        self._set_bounds(bounds, P)
         self.k_cache[:, :, :P].copy_(keys[:, :, :P])
         self.v_cache[:, :, :P].copy_(values[:, :, :P])
         self.plen.fill_(P)
         self.gen_count.zero_()
         self.gen_sum.zero_()
         self.max_prompt = P
-        self.max_chunks = (P + self.block - 1) // self.block
+        self.max_chunks = max(self.chunk_counts)
         self.steps = 0
         st = _lib.stream_handle()
         _lib.call("dhsa_centroids", self.code, _lib.ptr(self.k_cache), self.L_cap * self.D,
@@ -248,10 +282,9 @@ class SparseDecoder:
         (fp64 centroids + selected K/V rows + q/o)."""
         esz = torch.finfo(self.dtype).bits // 8
         P, g = self.max_prompt, self.steps
-        nc = (P + self.block - 1) // self.block
         # centroid stream: fp16 sketch (the fp64 re-scoring of the few chunks
         # at the cut is not counted) or fp64 centroids
-        cent = self.U * nc * self.D * (2 if self.scoring == "sketch" else 8)
+        cent = sum(self.chunk_counts) * self.D * (2 if self.scoring == "sketch" else 8)
         sel_tokens = min(self.budget, P + g + 1)
         per_sel = sel_tokens * self.D * esz * 2
         kv = (self.items if self.per_head else self.U) * per_sel

@@ -18,6 +18,8 @@ group.npz     group-shared decode rows: mask_from_chunk_scores over the
               head-aggregated S_c (harness.py:288-306) on extend_for_decode
               bounds, agg = max and mean, 4 heads sharing one key set (GQA)
 centroids.npz aggregate_rows (chunk_repr.py:57-68), bitwise
+nms.npz       nms_boundaries (chunking.py:57-89) on 300 random score vectors
+              incl. forced ties, with random min_conf / window / max_chunks
 c1.npz        the C1 demo shape (L=4096, 8 heads, d=64, block 64, top-k 16,
               budget 1025): 3 decode steps per head, fp32-valued inputs,
               rows stored as (start, count) ranges + attention outputs
@@ -33,7 +35,7 @@ sys.dont_write_bytecode = True
 sys.path.insert(0, "/root/reference/pkg/src")
 
 from dhsa.chunk_repr import aggregate_rows, build_chunk_reps, chunk_similarity  # noqa: E402
-from dhsa.chunking import extend_for_decode, static_boundaries  # noqa: E402
+from dhsa.chunking import extend_for_decode, nms_boundaries, static_boundaries  # noqa: E402
 from dhsa.core import TokenSequence, dense_attention  # noqa: E402
 from dhsa.masks import DecodeSession, mask_from_chunk_scores, prefill_mask, topk_row  # noqa: E402
 
@@ -193,6 +195,27 @@ def gen_centroids():
     save_records("centroids.npz", recs)
 
 
+def gen_nms():
+    rng = np.random.default_rng(11)
+    scores, params, outs = [], [], []
+    for _ in range(300):
+        length = int(rng.integers(1, 60))
+        sc = rng.random(length)
+        if rng.random() < 0.3:
+            sc = np.round(sc, 1)  # forced ties
+        min_conf = float(rng.choice([0.0, 0.1, 0.3, 0.5]))
+        window = int(rng.integers(0, 9))
+        max_chunks = int(rng.integers(1, 8))
+        scores.append(sc)
+        params.append((min_conf, window, max_chunks))
+        outs.append(nms_boundaries(sc, min_conf, window, max_chunks))
+    flat, so = pack_rows([np.asarray(x) for x in scores])
+    flat = np.concatenate(scores)
+    ov, oo = pack_rows(outs)
+    np.savez_compressed(os.path.join(OUT, "nms.npz"), scores=flat, score_off=so,
+                        params=np.array(params, dtype=np.float64), bounds=ov, bounds_off=oo)
+
+
 def c1_inputs(seed=7):
     """C1 demo shape; regenerated identically by tests (numpy PCG64)."""
     rng = np.random.default_rng(seed)
@@ -238,10 +261,15 @@ def gen_c1():
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 1:  # regenerate selected fixtures only, e.g. `nms`
+        for name in sys.argv[1:]:
+            globals()[f"gen_{name}"]()
+        sys.exit(0)
     gen_topk()
     gen_decode()
     gen_prefill()
     gen_group()
     gen_centroids()
     gen_c1()
+    gen_nms()
     print("golden fixtures written to", OUT)

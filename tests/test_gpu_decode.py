@@ -199,3 +199,57 @@ def test_attention_modes(mode, hint):
         dec.tiles_hint = hint
     worst = run_and_check(dec, t, host, P, steps, "max")
     assert worst <= TOL[torch.bfloat16], worst
+
+
+def _random_bounds(rng, P, lo=1, hi=150):
+    """Dynamic (NMS-like) boundaries: chunks of random length in [lo, hi]."""
+    b = [0]
+    while b[-1] < P:
+        b.append(min(P, b[-1] + int(rng.integers(lo, hi + 1))))
+    return b
+
+
+@pytest.mark.parametrize("dtype,agg", [(torch.bfloat16, "max"), (torch.bfloat16, "none"),
+                                       (torch.float32, "mean")])
+def test_dynamic_boundaries(dtype, agg):
+    """variable-length chunks (one boundary list per unit,
+    short and longer-than-a-tile chunks) through the batched engine; every
+    selection exact against DecodeSession semantics on the same bounds."""
+    B, Hq, Hkv, D, P, steps = 2, 8, 2, 128, 2500, 4
+    rng = np.random.default_rng(31)
+    bounds = [_random_bounds(rng, P) for _ in range(B * Hkv)]
+    t, host = make_inputs(B, Hq, Hkv, D, P, steps, dtype, seed=32)
+    dec = _dec(batch=B, q_heads=Hq, kv_heads=Hkv, head_dim=D, max_len=P + steps, block=64,
+               budget=700, dtype=dtype, agg=agg, max_chunks=max(len(b) for b in bounds))
+    dec.prefill(t["k"][:, :, :P].cuda(), t["v"][:, :, :P].cuda(), bounds=bounds)
+    G = Hq // Hkv
+    oracles = {}
+    for u in range(B * Hkv):
+        b, h = divmod(u, Hkv)
+        n = G if agg == "none" else 1
+        oracles[u] = [O.DecodeOracle(host["k"][b, h, :P], bounds[u], dec.budget) for _ in range(n)]
+    worst = 0.0
+    for s in range(steps):
+        pos = P + s
+        out = dec.step(t["q"][:, :, s].contiguous().cuda(), t["k"][:, :, pos].contiguous().cuda(),
+                       t["v"][:, :, pos].contiguous().cuda())
+        torch.cuda.synchronize()
+        sel = dec.selection()
+        o = out.double().cpu().numpy()
+        for u in range(B * Hkv):
+            b, h = divmod(u, Hkv)
+            qh = host["q"][b, h * G:(h + 1) * G, s]
+            kk = host["k"][b, h, pos]
+            if agg == "none":
+                rows = [oracles[u][j].step(qh[j], kk) for j in range(G)]
+                for j in range(G):
+                    assert np.array_equal(tiles_to_idx(sel[u * G + j]), rows[j]), (s, u, j)
+            else:
+                row = oracles[u][0].step_group(qh, kk, agg=agg)
+                rows = [row] * G
+                assert np.array_equal(tiles_to_idx(sel[u]), row), (s, u)
+            for j in range(G):
+                ref = O.attend_row(qh[j], host["k"][b, h, :pos + 1], host["v"][b, h, :pos + 1],
+                                   rows[j])
+                worst = max(worst, np.abs(o[b, h * G + j] - ref).max() / np.abs(ref).max())
+    assert worst <= TOL[dtype], worst

@@ -170,3 +170,23 @@ def test_no_oracle_import_in_product():
             if f.endswith(".py"):
                 src = open(os.path.join(root, f)).read()
                 assert "oracle" not in src.replace("oracle/", ""), f
+
+
+def test_nms_boundaries_golden():
+    """nms_boundaries (chunking.py:57-89) against the reference's own outputs
+    on 300 random score vectors with ties (tests/golden/nms.npz)."""
+    import golden_io as GI
+
+    z = GI.load("nms.npz")
+    scores = GI.unpack_rows(z["scores"], z["score_off"])
+    outs = GI.unpack_rows(z["bounds"], z["bounds_off"])
+    for sc, (min_conf, window, max_chunks), want in zip(scores, z["params"], outs):
+        got = P.nms_boundaries(sc, float(min_conf), int(window), int(max_chunks))
+        assert got == [int(x) for x in want]
+    assert P.nms_boundaries(np.zeros(16)) == [0, 16]
+    with pytest.raises(ValueError):
+        P.nms_boundaries(np.zeros(0))
+    with pytest.raises(ValueError):
+        P.nms_boundaries([0.5, np.nan])
+    with pytest.raises(ValueError):
+        P.nms_boundaries([0.5], max_chunks=0)
