@@ -364,18 +364,20 @@ __device__ __forceinline__ double agg_d(const double* v, int nh) {
 // total weight.  Replaces a 4-pass 8-bit radix select (~7 us -> ~2 us).
 constexpr int kHistBins = 1024;
 __device__ __forceinline__ int hpad(int b) { return b + (b >> 5); }  // bank-conflict-free scan
+template <int NT>
 struct HistShared {
   uint32_t hist[kHistBins + kHistBins / 32];
-  float wmin[kSelectThreads / 32], wmax[kSelectThreads / 32];
+  float wmin[NT / 32], wmax[NT / 32];
 };
 
+template <int NT>
 __device__ int hist_threshold(const uint32_t* ak, const int32_t* lens, int n, uint32_t R,
-                              HistShared& hs, double& vmin, double& bscale) {
-  constexpr int NW = kSelectThreads / 32;
+                              HistShared<NT>& hs, double& vmin, double& bscale) {
+  constexpr int NW = NT / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int b = tid; b < kHistBins + kHistBins / 32; b += kSelectThreads) hs.hist[b] = 0;
+  for (int b = tid; b < kHistBins + kHistBins / 32; b += NT) hs.hist[b] = 0;
   float mn = INFINITY, mx = -INFINITY;
-  for (int c = tid; c < n; c += kSelectThreads)
+  for (int c = tid; c < n; c += NT)
     if (lens[c] > 0) {
       const float v = key32_value(ak[c]);
       mn = fminf(mn, v);
@@ -398,7 +400,7 @@ __device__ int hist_threshold(const uint32_t* ak, const int32_t* lens, int n, ui
   }
   vmin = (double)mn;
   bscale = mx > mn ? ((double)kHistBins - 0.5) / ((double)mx - (double)mn) : 0.0;
-  for (int c = tid; c < n; c += kSelectThreads) {
+  for (int c = tid; c < n; c += NT) {
     const int len = lens[c];
     if (len > 0) {
       const double f = floor(((double)key32_value(ak[c]) - vmin) * bscale);
@@ -441,16 +443,16 @@ __device__ int hist_threshold(const uint32_t* ak, const int32_t* lens, int n, ui
 // The global walk (splitkv.cu) over the candidates of all shards then equals
 // the unsharded walk: a chunk with a positive global take has fewer than R
 // tokens ranked above it globally, hence locally, so it is a local candidate.
-template <int D, int G, int AGG>
+template <int D, int G, int AGG, int NT>
 __device__ void emit_candidates(const SketchArgs& a, const UnitChunks& uc, const int32_t* takes,
                                 int32_t* list, int n, int s, const double (*qd)[D], int h0, int nh,
                                 double gex, int u) {
-  constexpr int NW = kSelectThreads / 32;
+  constexpr int NW = NT / 32;
   __shared__ int s_ncand;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) s_ncand = 0;
   __syncthreads();
-  for (int c = tid; c < n; c += kSelectThreads)
+  for (int c = tid; c < n; c += NT)
     if (takes[c] > 0) list[atomicAdd(&s_ncand, 1)] = c;
   __syncthreads();
   const int nc = s_ncand;
@@ -492,15 +494,15 @@ __device__ void emit_candidates(const SketchArgs& a, const UnitChunks& uc, const
   __syncthreads();
 }
 
-template <int D, int G, int AGG>
-__global__ __launch_bounds__(kSelectThreads) void sketch_select_kernel(SketchArgs a) {
-  constexpr int NW = kSelectThreads / 32;
+template <int D, int G, int AGG, int NT>
+__global__ __launch_bounds__(NT) void sketch_select_kernel(SketchArgs a) {
+  constexpr int NW = NT / 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ WalkShared sh;
   __shared__ double qd[G][D];
   __shared__ double s_qn[G], s_gen[G];
   __shared__ int s_nunc, s_win;
-  __shared__ HistShared hs;
+  __shared__ HistShared<NT> hs;
 
   const int u = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -513,7 +515,7 @@ __global__ __launch_bounds__(kSelectThreads) void sketch_select_kernel(SketchArg
   pdl_trigger();  // the attention kernel may launch once every select CTA is resident
   DBG_T(0);
   // ---- prologue: every global load of the step issued before one barrier ----
-  for (int i = tid; i < G * D; i += kSelectThreads)
+  for (int i = tid; i < G * D; i += NT)
     qd[i / D][i % D] = to_f64(a.q[(int64_t)u * G * D + i]);
   const int g = a.gen_count[u];
   const int gl = (a.split && !a.owns_tail) ? 0 : g;  // generated tokens held by this shard
@@ -613,19 +615,19 @@ __global__ __launch_bounds__(kSelectThreads) void sketch_select_kernel(SketchArg
       // batched: the approximate scores (L2) are loaded before any smem store
       constexpr int UNR = 4;
       const float gkey = (float)(gex * scale);
-      for (int c0 = tid; c0 < n; c0 += UNR * kSelectThreads) {
+      for (int c0 = tid; c0 < n; c0 += UNR * NT) {
         float v[UNR];
         int ln[UNR];
 #pragma unroll
         for (int k = 0; k < UNR; ++k) {
-          const int c = c0 + k * kSelectThreads;
+          const int c = c0 + k * NT;
           v[k] = (c < uc.nc) ? __ldcg(apx + c) : gkey;
           int lo;
           if (c < n) uc.chunk(c, lo, ln[k]);
         }
 #pragma unroll
         for (int k = 0; k < UNR; ++k) {
-          const int c = c0 + k * kSelectThreads;
+          const int c = c0 + k * NT;
           if (c < n) {
             lens[c] = ln[k];
             ak[c] = order_key32(v[k]);
@@ -656,7 +658,7 @@ __global__ __launch_bounds__(kSelectThreads) void sketch_select_kernel(SketchArg
         return f < 0.0 ? 0 : (f > (double)(kHistBins - 1) ? kHistBins - 1 : (int)f);
       };
       int win_local = 0;
-      for (int c = tid; c < n; c += kSelectThreads) {
+      for (int c = tid; c < n; c += NT) {
         const double v = (double)key32_value(ak[c]);
         uint64_t k;
         // bin() is monotone: bin(v - 2E) > b* => v - 2E exceeds every score of
@@ -708,7 +710,7 @@ __global__ __launch_bounds__(kSelectThreads) void sketch_select_kernel(SketchArg
         // exact walk over the uncertain chunks: rank by (fp64 desc, chunk asc)
         const int rp = (int)R - s_win;
         int32_t* take = reinterpret_cast<int32_t*>(ak);  // approx keys no longer needed
-        for (int i = tid; i < nu; i += kSelectThreads) {
+        for (int i = tid; i < nu; i += NT) {
           const int ci = unc[i];
           const uint64_t ki = key64[ci];
           int before = 0;
@@ -721,30 +723,30 @@ __global__ __launch_bounds__(kSelectThreads) void sketch_select_kernel(SketchArg
           take[i] = rem <= 0 ? 0 : (rem < lens[ci] ? rem : lens[ci]);
         }
         __syncthreads();
-        for (int c = tid; c < n; c += kSelectThreads)
+        for (int c = tid; c < n; c += NT)
           if (key64[c] != ~0ull) lens[c] = 0;
         __syncthreads();
-        for (int i = tid; i < nu; i += kSelectThreads) lens[unc[i]] = take[i];
+        for (int i = tid; i < nu; i += NT) lens[unc[i]] = take[i];
         __syncthreads();
         DBG_T(6);
         if (!a.split)
-          emit_takes<kSelectThreads>(uc, lens, n, row, a.tile_tokens,
+          emit_takes<NT>(uc, lens, n, row, a.tile_tokens,
                                      a.tiles + (int64_t)s * a.tile_cap * 2, a.tile_cap,
                                      a.ntiles + s, sh);
         DBG_T(7);
         done = true;
       } else {
-        radix_threshold<kSelectThreads, uint64_t>(key64, lens, n, R, sh, prefix, mask, rrem);
+        radix_threshold<NT, uint64_t>(key64, lens, n, R, sh, prefix, mask, rrem);
       }
     }
     if (!done && a.split)
-      walk_takes<kSelectThreads, uint64_t>(key64, lens, n, R, prefix, mask, rrem, sh);
+      walk_takes<NT, uint64_t>(key64, lens, n, R, prefix, mask, rrem, sh);
     else if (!done)
-      walk_emit<kSelectThreads, uint64_t>(uc, key64, lens, n, R, prefix, mask, rrem, row,
+      walk_emit<NT, uint64_t>(uc, key64, lens, n, R, prefix, mask, rrem, row,
                                           a.tile_tokens, a.tiles + (int64_t)s * a.tile_cap * 2,
                                           a.tile_cap, a.ntiles + s, sh);
     if (a.split)
-      emit_candidates<D, G, AGG>(a, uc, lens, unc, n, s, qd, h0, nh, gex, u);
+      emit_candidates<D, G, AGG, NT>(a, uc, lens, unc, n, s, qd, h0, nh, gex, u);
   }
   __syncthreads();
   if (tid == 0) {
@@ -837,7 +839,10 @@ static int launch_step(const SketchArgs& a, int U, size_t sel_smem, cudaStream_t
   score<<<(unsigned)grid, kTcThreads, ring, s>>>(tm, a);
   rc = check_launch("dhsa_decode_step_bf16(score)");
   if (rc) return rc;
-  auto sel = sketch_select_kernel<D, G, AGG>;
+  // a wider CTA for very long units (e.g. 16K chunks in one split-KV shard)
+  auto sel = a.n_max > 4096 ? sketch_select_kernel<D, G, AGG, 1024>
+                            : sketch_select_kernel<D, G, AGG, kSelectThreads>;
+  const int sel_threads = a.n_max > 4096 ? 1024 : kSelectThreads;
   {  // static + dynamic may exceed the 48 KB default even for small dynamic sizes
     e = cudaFuncSetAttribute(sel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel_smem);
     if (e != cudaSuccess) {
@@ -847,7 +852,7 @@ static int launch_step(const SketchArgs& a, int U, size_t sel_smem, cudaStream_t
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)U);
-  cfg.blockDim = dim3(kSelectThreads);
+  cfg.blockDim = dim3(sel_threads);
   cfg.dynamicSmemBytes = sel_smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];

@@ -12,12 +12,19 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 32
 L = int(sys.argv[2]) if len(sys.argv) > 2 else 131072
+SPLIT = len(sys.argv) > 3 and sys.argv[3] == "split"  # C4 path: one shard, LocalComm
 Hq, Hkv, D = 32, 8, 128
 dbg = torch.zeros(262144, dtype=torch.int64, device="cuda")
 os.environ["DHSA_DEBUG_TIMING"] = str(dbg.data_ptr())
 from paper_2510_24606_b200.decode import SparseDecoder  # noqa: E402
 
-dec = SparseDecoder(B, Hq, Hkv, D, L + 64, block=64, top_k=64, dtype=torch.bfloat16, agg="max")
+if SPLIT:
+    from paper_2510_24606_b200.splitkv import LocalComm, SplitKVShard
+
+    shard = SplitKVShard(B, Hq, Hkv, D, L, rank=0, world=1, top_k=64, max_new=64)
+    dec = shard.dec
+else:
+    dec = SparseDecoder(B, Hq, Hkv, D, L + 64, block=64, top_k=64, dtype=torch.bfloat16, agg="max")
 g = torch.Generator(device="cuda")
 g.manual_seed(0)
 for t in (dec.k_cache, dec.v_cache):
@@ -27,12 +34,19 @@ q = torch.randn(B, Hq, D, device="cuda", generator=g).bfloat16()
 k = torch.randn(B, Hkv, D, device="cuda", generator=g).bfloat16()
 v = torch.randn(B, Hkv, D, device="cuda", generator=g).bfloat16()
 out = torch.empty(B, Hq, D, dtype=torch.bfloat16, device="cuda")
-dec.step(q, k, v, out=out)
+if SPLIT:
+    comm = LocalComm()
+    shard.step(q, k, v, comm, out=out)
+else:
+    dec.step(q, k, v, out=out)
 torch.cuda.synchronize()
 s = torch.cuda.Stream()
 gr = torch.cuda.CUDAGraph()
 with torch.cuda.graph(gr, stream=s):
-    dec.launch(q, k, v, out, stream=s)
+    if SPLIT:
+        shard.launch(q, k, v, comm, out, stream=s)
+    else:
+        dec.launch(q, k, v, out, stream=s)
 for _ in range(5):
     gr.replay()
 torch.cuda.synchronize()
@@ -63,8 +77,9 @@ def show(name, col):
 print(f"graph replay (events): {e0.elapsed_time(e1) * 1e3:.1f} us")
 show("sketch CTA start", sk[:, 0])
 show("sketch CTA end", sk[:, 1])
-for k_, n in [(0, "select start"), (1, "select after pdl_wait"), (3, "select after radix"),
-              (4, "select classified"), (7, "select emitted"), (8, "select end")]:
+for k_, n in [(0, "select start"), (1, "select after pdl_wait"), (2, "select keys loaded"),
+              (3, "select after threshold"), (4, "select classified"), (5, "select rescored"),
+              (6, "select exact walk"), (7, "select emitted"), (8, "select end")]:
     show(n, sel[:, k_])
 show("attn CTA start", at[:, 0])
 show("attn first tile", at[:, 1])
