@@ -325,11 +325,7 @@ def run_gpu(args):
         for i in range(ne + 1):
             if i == 1:
                 e0.record(stream)
-            dq.copy_(hq, non_blocking=True)
-            dk.copy_(hk, non_blocking=True)
-            dv.copy_(hv, non_blocking=True)
-            dec.step(dq, dk, dv, out=out)
-            hout.copy_(out, non_blocking=True)
+            dec.step_host(hq, hk, hv, hout)
         e1.record(stream)
         torch.cuda.synchronize()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / ne, world)
@@ -358,7 +354,8 @@ def run_gpu(args):
         "breakdown_us": us,
         "e2e": {"value": B * world / (e2e_ms / 1e3), "unit": "tokens/s",
                 "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "path": "SparseDecoder.step (ctypes C-ABI) with pinned host q/k/v -> o"},
+                "path": "SparseDecoder.step_host (public API: pinned host q/k/v -> static device "
+                        "buffers -> one CUDA-graph replay of the C-ABI kernels -> host o)"},
         "gpu_launches": dec.kernels_per_step * S,
         "clocks": clk.summary(),
         "splits": dec.splits if dec.attn_mode == "split" else None,

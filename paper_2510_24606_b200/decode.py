@@ -197,6 +197,39 @@ class SparseDecoder:
         self.steps += 1
         return out
 
+    def step_host(self, q, k_new, v_new, out):
+        """Serving entry point: one decode step from HOST tensors (pinned for
+        asynchronous copies) to a host output, replaying one captured CUDA
+        graph of the step's kernels.  q [B, Hq, D], k_new/v_new [B, Hkv, D],
+        out [B, Hq, D] in the cache dtype.  Inputs go to static device
+        buffers (the graph's arguments); every step-dependent value
+        (generated count, running sum, flags) lives in device memory, so one
+        graph serves every step.  The copies, the graph and the output copy
+        are ordered on the current stream; returns ``out`` (valid once that
+        stream is synchronised)."""
+        if self.max_prompt + self.steps + 1 > self.L_cap - 64:
+            raise RuntimeError("KV cache capacity exhausted")
+        if getattr(self, "_graph", None) is None:
+            kw = dict(dtype=self.dtype, device=self.dev)
+            self._gq = torch.empty(self.B, self.Hq, self.D, **kw)
+            self._gk = torch.empty(self.B, self.Hkv, self.D, **kw)
+            self._gv = torch.empty(self.B, self.Hkv, self.D, **kw)
+            self._go = torch.empty(self.B, self.Hq, self.D, **kw)
+            # warm every kernel module outside capture without advancing state
+            self._graph = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.graph(self._graph, stream=side):
+                self.launch(self._gq, self._gk, self._gv, self._go, stream=side)
+            torch.cuda.current_stream().wait_stream(side)
+        self._gq.copy_(q, non_blocking=True)
+        self._gk.copy_(k_new, non_blocking=True)
+        self._gv.copy_(v_new, non_blocking=True)
+        self._graph.replay()
+        out.copy_(self._go, non_blocking=True)
+        self.steps += 1
+        return out
+
     def launch(self, q, k_new, v_new, out, stream=None):
         """Enqueue one step (graph-capturable): 3 kernels with sketch scoring
         (sketch stream, select + state update, attention), 4 with fp64 scoring."""

@@ -253,3 +253,32 @@ def test_dynamic_boundaries(dtype, agg):
                                    rows[j])
                 worst = max(worst, np.abs(o[b, h * G + j] - ref).max() / np.abs(ref).max())
     assert worst <= TOL[dtype], worst
+
+
+def test_step_host_graph_equals_eager():
+    """The serving entry point (host buffers, one captured CUDA graph reused
+    for every step) gives bit-identical selections and outputs to eager steps."""
+    B, Hq, Hkv, D, P, steps = 2, 8, 2, 128, 2000, 4
+    t, _ = make_inputs(B, Hq, Hkv, D, P, steps, torch.bfloat16, seed=41)
+    res = []
+    for mode in ("eager", "graph"):
+        dec = _dec(batch=B, q_heads=Hq, kv_heads=Hkv, head_dim=D, max_len=P + steps, block=64,
+                   top_k=6, dtype=torch.bfloat16, agg="max")
+        dec.prefill(t["k"][:, :, :P].cuda(), t["v"][:, :, :P].cuda())
+        outs = []
+        for s in range(steps):
+            q = t["q"][:, :, s].contiguous()
+            k = t["k"][:, :, P + s].contiguous()
+            v = t["v"][:, :, P + s].contiguous()
+            if mode == "eager":
+                o = dec.step(q.cuda(), k.cuda(), v.cuda()).cpu()
+            else:
+                o = torch.empty(B, Hq, D, dtype=torch.bfloat16).pin_memory()
+                dec.step_host(q.pin_memory(), k.pin_memory(), v.pin_memory(), o)
+                torch.cuda.synchronize()
+            outs.append((o.clone(), [x.copy() for x in dec.selection()]))
+        res.append(outs)
+    for (oa, sa), (ob, sb) in zip(*res):
+        assert torch.equal(oa, ob)
+        for a, b in zip(sa, sb):
+            assert np.array_equal(a, b)
