@@ -282,3 +282,18 @@ def test_step_host_graph_equals_eager():
         assert torch.equal(oa, ob)
         for a, b in zip(sa, sb):
             assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("D,G,agg", [(64, 4, "max"), (64, 8, "none"), (128, 8, "max"),
+                                     (128, 1, "max"), (64, 2, "mean")])
+def test_bf16_head_dims_and_groups(D, G, agg):
+    """bf16 sketch + stream attention across head dims {64, 128} and group
+    sizes {1, 2, 4, 8} (template instantiations of every decode kernel)."""
+    B, Hkv, P, steps = 2, 2, 1500, 3
+    Hq = G * Hkv
+    t, host = make_inputs(B, Hq, Hkv, D, P, steps, torch.bfloat16, seed=50 + D + G)
+    dec = _dec(batch=B, q_heads=Hq, kv_heads=Hkv, head_dim=D, max_len=P + steps, block=64,
+               top_k=5, dtype=torch.bfloat16, agg=agg)
+    assert dec.scoring == "sketch" and dec.attn_mode == "stream"
+    worst = run_and_check(dec, t, host, P, steps, agg)
+    assert worst <= TOL[torch.bfloat16], worst
