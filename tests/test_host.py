@@ -190,3 +190,31 @@ def test_nms_boundaries_golden():
         P.nms_boundaries([0.5, np.nan])
     with pytest.raises(ValueError):
         P.nms_boundaries([0.5], max_chunks=0)
+
+
+@pytest.mark.skipif(__import__("torch").cuda.is_available(), reason="checks the no-GPU path")
+def test_engines_refuse_without_gpu():
+    """No CPU fallback: every batched engine raises without a CUDA device."""
+    from paper_2510_24606_b200.decode import SparseDecoder
+    from paper_2510_24606_b200.prefill import SparsePrefill
+    from paper_2510_24606_b200.splitkv import SplitKVShard
+
+    with pytest.raises(RuntimeError, match="CUDA"):
+        SparseDecoder(1, 4, 1, 128, 256)
+    with pytest.raises(RuntimeError, match="CUDA"):
+        SparsePrefill(1, 4, 1, 128, 256)
+    with pytest.raises(RuntimeError, match="CUDA"):
+        SplitKVShard(1, 4, 1, 128, 256, rank=0, world=1)
+
+
+def test_c_abi_new_entry_points_exported():
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    for name in ("dhsa_attn_stream", "dhsa_attn_stream_workspace_size", "dhsa_attn_stream_counters",
+                 "dhsa_prefill_scores", "dhsa_prefill_plan", "dhsa_prefill_plan_capacity",
+                 "dhsa_prefill_attn", "dhsa_decode_candidates_bf16", "dhsa_split_select",
+                 "dhsa_attn_partials", "dhsa_merge_partials"):
+        assert hasattr(lib, name), name
+    lib.dhsa_prefill_plan_capacity.restype = ctypes.c_int
+    lib.dhsa_prefill_plan_capacity.argtypes = [ctypes.c_int64, ctypes.c_int]
+    assert lib.dhsa_prefill_plan_capacity(4097, 64) == 66
+    assert lib.dhsa_prefill_plan_capacity(0, 64) == -1
