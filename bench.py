@@ -313,8 +313,8 @@ def run_gpu(args):
     traffic = load_traffic().get(name, {}).get(dominant)
 
     # end-to-end through the public API with pinned host buffers
-    pin = lambda t: t[0].cpu().pin_memory()  # noqa: E731
-    hq, hk, hv = pin(qs), pin(ks), pin(vs)
+    # one pinned host buffer per step input set: [q | k | v] (one H2D copy)
+    hqkv = torch.cat([qs[0].reshape(-1), ks[0].reshape(-1), vs[0].reshape(-1)]).cpu().pin_memory()
     hout = torch.empty(B, Hq, D, dtype=dtype).pin_memory()
     dq, dk, dv = torch.empty_like(qs[0]), torch.empty_like(ks[0]), torch.empty_like(vs[0])
     ne = args.e2e_steps
@@ -325,7 +325,7 @@ def run_gpu(args):
         for i in range(ne + 1):
             if i == 1:
                 e0.record(stream)
-            dec.step_host(hq, hk, hv, hout)
+            dec.step_host_packed(hqkv, hout)
         e1.record(stream)
         torch.cuda.synchronize()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / ne, world)
@@ -354,8 +354,9 @@ def run_gpu(args):
         "breakdown_us": us,
         "e2e": {"value": B * world / (e2e_ms / 1e3), "unit": "tokens/s",
                 "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "path": "SparseDecoder.step_host (public API: pinned host q/k/v -> static device "
-                        "buffers -> one CUDA-graph replay of the C-ABI kernels -> host o)"},
+                "path": "SparseDecoder.step_host_packed (public API: one pinned host [q|k|v] "
+                        "buffer -> one H2D copy -> one CUDA-graph replay of the C-ABI kernels -> "
+                        "host o)"},
         "gpu_launches": dec.kernels_per_step * S,
         "clocks": clk.summary(),
         "splits": dec.splits if dec.attn_mode == "split" else None,

@@ -230,6 +230,37 @@ class SparseDecoder:
         self.steps += 1
         return out
 
+    def packed_layout(self):
+        """Element offsets of q / k_new / v_new in the packed step input of
+        ``step_host_packed`` ([q | k | v], cache dtype)."""
+        nq, nk = self.B * self.Hq * self.D, self.B * self.Hkv * self.D
+        return (0, nq), (nq, nq + nk), (nq + nk, nq + 2 * nk)
+
+    def step_host_packed(self, qkv, out):
+        """``step_host`` with the step's inputs packed in ONE pinned host
+        tensor [q | k_new | v_new] (flattened, cache dtype): one host->device
+        copy per step instead of three."""
+        if self.max_prompt + self.steps + 1 > self.L_cap - 64:
+            raise RuntimeError("KV cache capacity exhausted")
+        (q0, q1), (k0, k1), (v0, v1) = self.packed_layout()
+        if getattr(self, "_pgraph", None) is None:
+            self._pin = torch.empty(v1, dtype=self.dtype, device=self.dev)
+            self._po = torch.empty(self.B, self.Hq, self.D, dtype=self.dtype, device=self.dev)
+            q = self._pin[q0:q1].view(self.B, self.Hq, self.D)
+            k = self._pin[k0:k1].view(self.B, self.Hkv, self.D)
+            v = self._pin[v0:v1].view(self.B, self.Hkv, self.D)
+            self._pgraph = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.graph(self._pgraph, stream=side):
+                self.launch(q, k, v, self._po, stream=side)
+            torch.cuda.current_stream().wait_stream(side)
+        self._pin.copy_(qkv.view(-1), non_blocking=True)
+        self._pgraph.replay()
+        out.copy_(self._po, non_blocking=True)
+        self.steps += 1
+        return out
+
     def launch(self, q, k_new, v_new, out, stream=None):
         """Enqueue one step (graph-capturable): 3 kernels with sketch scoring
         (sketch stream, select + state update, attention), 4 with fp64 scoring."""

@@ -297,3 +297,28 @@ def test_bf16_head_dims_and_groups(D, G, agg):
     assert dec.scoring == "sketch" and dec.attn_mode == "stream"
     worst = run_and_check(dec, t, host, P, steps, agg)
     assert worst <= TOL[torch.bfloat16], worst
+
+
+def test_step_host_packed_equals_eager():
+    """One packed pinned [q|k|v] host buffer per step gives the eager results."""
+    B, Hq, Hkv, D, P, steps = 2, 8, 2, 128, 1500, 3
+    t, _ = make_inputs(B, Hq, Hkv, D, P, steps, torch.bfloat16, seed=43)
+    res = []
+    for mode in ("eager", "packed"):
+        dec = _dec(batch=B, q_heads=Hq, kv_heads=Hkv, head_dim=D, max_len=P + steps, block=64,
+                   top_k=5, dtype=torch.bfloat16, agg="max")
+        dec.prefill(t["k"][:, :, :P].cuda(), t["v"][:, :, :P].cuda())
+        outs = []
+        for s in range(steps):
+            q, k, v = (t[n][:, :, s if n == "q" else P + s].contiguous() for n in ("q", "k", "v"))
+            if mode == "eager":
+                o = dec.step(q.cuda(), k.cuda(), v.cuda()).cpu()
+            else:
+                qkv = torch.cat([q.reshape(-1), k.reshape(-1), v.reshape(-1)]).pin_memory()
+                o = torch.empty(B, Hq, D, dtype=torch.bfloat16).pin_memory()
+                dec.step_host_packed(qkv, o)
+                torch.cuda.synchronize()
+            outs.append(o.clone())
+        res.append(outs)
+    for a, b in zip(*res):
+        assert torch.equal(a, b)
