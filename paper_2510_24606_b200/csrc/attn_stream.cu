@@ -297,10 +297,18 @@ __global__ __launch_bounds__(192, 2) void attn_stream_kernel(const __grid_consta
 template <int D>
 __global__ __launch_bounds__(D) void stream_merge_kernel(StreamArgs a) {
   constexpr int REC = D + 2;
+  const int item = blockIdx.x, h = blockIdx.y, d = threadIdx.x, GH = a.GH;
+  // read the item's tile count (and decide whether it needs a merge at all)
+  // before waiting for the attention grid: it is final once the item's ready
+  // flag is up (without flags the select grid completed before the attention
+  // grid was launched)
+  if (a.ready) {
+    if (threadIdx.x == 0) spin_geq(a.ready + item, 1);
+    __syncthreads();
+  }
+  const int nt = __ldcg(a.ntiles + item);
   pdl_wait();
   if (a.dbg && threadIdx.x == 0) atomicMin(a.dbg + kDbgAttn + 8192, gtimer());
-  const int item = blockIdx.x, h = blockIdx.y, d = threadIdx.x, GH = a.GH;
-  const int nt = __ldcg(a.ntiles + item);
   int lo, hi;
   int S, nseg;
   seg_shape(a, item, S, nseg);
