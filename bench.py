@@ -179,13 +179,21 @@ def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU; ranks beyond the visible devices wrap around (only
+    # for exercising the multi-rank path on a smaller box, with
+    # DHSA_DIST_BACKEND=gloo since NCCL refuses two ranks on one device)
+    dev = local % max(1, torch.cuda.device_count()) if torch.cuda.is_available() else 0
     if world > 1 and not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        torch.cuda.set_device(dev)
+        backend = os.environ.get("DHSA_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     elif torch.cuda.is_available():
-        torch.cuda.set_device(local)
-    return world, rank, local
+        torch.cuda.set_device(dev)
+    return world, rank, dev
 
 
 def barrier(world):
