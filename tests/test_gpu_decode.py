@@ -322,3 +322,14 @@ def test_step_host_packed_equals_eager():
         res.append(outs)
     for a, b in zip(*res):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("P", [1, 63, 65])
+def test_tiny_prompts(P):
+    """One-token prompt (a single chunk of length 1), ragged last chunks."""
+    B, Hq, Hkv, D, steps = 1, 4, 1, 128, 70  # the generated chunk outgrows a tile
+    t, host = make_inputs(B, Hq, Hkv, D, P, steps, torch.bfloat16, seed=70 + P)
+    dec = _dec(batch=B, q_heads=Hq, kv_heads=Hkv, head_dim=D, max_len=P + steps, block=64,
+               top_k=1, dtype=torch.bfloat16, agg="max")
+    worst = run_and_check(dec, t, host, P, steps, "max")
+    assert worst <= TOL[torch.bfloat16], worst

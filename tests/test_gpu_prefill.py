@@ -115,3 +115,10 @@ def test_prefill_4k_topk16():
     worst = _run(B=1, Hq=8, Hkv=2, L=4096, top_k=16, agg="max", seed=21,
                  check_rows=range(0, 4096, 31))
     assert worst <= TOL_BF16, worst
+
+
+@pytest.mark.parametrize("L", [1, 40, 64, 65, 130])
+def test_prefill_tiny_lengths(L):
+    """A single (short) chunk, exactly one block, one block + 1 token."""
+    worst = _run(B=1, Hq=4, Hkv=1, L=L, top_k=1, agg="max", seed=60 + L, check_rows=range(L))
+    assert worst <= TOL_BF16, worst

@@ -91,3 +91,10 @@ def test_splitkv_budget_edges(budget):
     worst = _run(2, B=1, Hq=4, Hkv=1, D=128, P=1500, steps=3, top_k=1, agg="max",
                  budget=budget, seed=7)
     assert worst <= TOL[torch.bfloat16], worst
+
+
+def test_splitkv_ragged_prompt():
+    """Prompt length not a multiple of the block: the last shard's last chunk
+    is short; 3 shards."""
+    worst = _run(3, B=1, Hq=4, Hkv=1, D=128, P=3001, steps=3, top_k=5, agg="max", seed=9)
+    assert worst <= TOL[torch.bfloat16], worst
