@@ -329,10 +329,14 @@ int dhsa_prefill_plan(const double* scores, int S, int n_chunks, int L, int bloc
 /* Block-sparse attention of every query row over its planned tokens:
  * softmax(K[idx] q / sqrt(D)) @ V[idx] (core.py:113-118) with tcgen05.mma
  * (bf16 operands from TMA-staged 128B-swizzled shared memory, fp32 TMEM
- * accumulators), one CTA per (plan, <= 4 q heads).  out [U*G][L][D] bf16. */
+ * accumulators, P kept in TMEM), per (plan, <= 4 q heads).  out [U*G][L][D]
+ * bf16.  counters: int32[2] zero at rest -> persistent grid (one CTA per SM
+ * pulling plans, TMEM / barriers / K-V ring kept across plans); NULL -> one
+ * CTA per (plan, head slice). */
 int dhsa_prefill_attn(const void* q, const void* k, const void* v, int U, int G, int L, int D,
                       int block, int agg, int64_t budget, const void* plans,
-                      const int32_t* nplan, int cap, void* out, dhsa_stream_t stream);
+                      const int32_t* nplan, int cap, void* out, int32_t* counters,
+                      dhsa_stream_t stream);
 
 /* f_upsample (masks.upsample, masks.py:87-100): out[i][j] = s[chunk(i)][chunk(j)]
  * for an n x n chunk-score matrix and bounds [n+1]; out is L x L fp64.  Only

@@ -37,6 +37,8 @@
 #include "tc05.cuh"
 #include "walk.cuh"
 
+#include <cstdlib>
+
 namespace dhsa {
 
 // ------------------------------------------------------------------- K7 --
@@ -194,6 +196,8 @@ struct PrefillArgs {
   int G, per_head, heads_per_cta, slices;
   __nv_bfloat16* out;  // [q heads][L][D]
   float scale_log2;
+  int S;               // selection rows
+  int32_t* counters;   // [2] plan pull counter, exits (persistent kernel); zero at rest
 };
 
 template <int MT, int NST>
@@ -475,6 +479,354 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_kernel(
   }
 }
 
+// Persistent variant: one CTA per SM pulls plans (heavy query chunks first)
+// from a device counter and keeps the TMEM allocation, the barriers and the
+// K/V ring alive across plans; the next plan's entries and Q tile load while
+// the current plan finishes (Q once its last S MMA has been issued, plan
+// entries double-buffered), and only the first PV of a plan waits for the
+// previous plan's epilogue to have read O.  Per-plan start-up (TMEM alloc,
+// Q and first K/V latency, epilogue) otherwise costs ~9 us per CTA.
+template <int MT, int NST>
+__global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_persist_kernel(
+    const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+    const __grid_constant__ CUtensorMap tmV, PrefillArgs a) {
+  using SM = PrefillSmem<MT, NST>;
+  constexpr int D = 128;
+  constexpr uint32_t kTmemCols = MT * 256;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t kv_full[NST], kv_empty[NST], s_full[2], p_full[2], o_done[2],
+      q_full, q_empty, o_free, plan_full[2], plan_empty[2];
+  __shared__ uint32_t s_tmem;
+  __shared__ int4 s_plan[2][288];
+  __shared__ int4 s_meta[2];  // (plan id or -1, entries, l, s * slices + hs)
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int total = a.S * a.nc * a.slices;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 4 * MT);
+      mbar_init(&o_done[i], 1);
+      mbar_init(&plan_full[i], 1);
+      mbar_init(&plan_empty[i], 1 + 4 * MT);
+    }
+    mbar_init(&q_full, 1);
+    mbar_init(&q_empty, 1);
+    mbar_init(&o_free, 4 * MT);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(&s_tmem, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = s_tmem;
+  const uint32_t sq = smem_u32(smem + SM::q_off);
+  const uint32_t skv = smem_u32(smem + SM::kv_off);
+  // plan p -> (query chunk l, selection row s, head slice hs), heavy first
+  auto decode = [&](int p, int& l, int& sr, int& hs) {
+    const int per_l = a.S * a.slices;
+    l = a.nc - 1 - p / per_l;
+    const int r = p - (a.nc - 1 - l) * per_l;
+    sr = r / a.slices;
+    hs = r - sr * a.slices;
+  };
+
+  if (warp == 0) {
+    // ------------------------------------------------ producer warp
+    if (lane == 0) {
+      prefetch_tmap(&tmQ);
+      prefetch_tmap(&tmK);
+      prefetch_tmap(&tmV);
+    }
+    int jg = 0, kq = 0;
+    for (int k = 0;; ++k) {
+      const int b = k & 1;
+      int p = 0;
+      if (lane == 0) p = atomicAdd(a.counters, 1);
+      p = __shfl_sync(0xffffffffu, p, 0);
+      if (k >= 2 && lane == 0) mbar_wait(&plan_empty[b], ((k >> 1) - 1) & 1);
+      __syncwarp();
+      if (p >= total) {
+        if (lane == 0) {
+          s_meta[b] = make_int4(-1, 0, 0, 0);
+          mbar_arrive(&plan_full[b]);
+        }
+        break;
+      }
+      int l, sr, hs;
+      decode(p, l, sr, hs);
+      const int np = __ldg(a.nplan + (int64_t)sr * a.nc + l);
+      const int4* plan = a.plans + ((int64_t)sr * a.nc + l) * a.cap;
+      for (int e = lane; e < np && e < 288; e += 32) s_plan[b][e] = __ldg(plan + e);
+      if (lane == 0) s_meta[b] = make_int4(p, np, l, sr * a.slices + hs);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&plan_full[b]);
+      if (np <= 0) continue;  // capacity overflow: reported by the host
+      if (lane == 0) {
+        const int unit = a.per_head ? sr / a.G : sr;
+        const int qh0 = (a.per_head ? sr : sr * a.G) + hs * a.heads_per_cta;
+        const int nh = a.per_head ? 1 : min(a.heads_per_cta, a.G - hs * a.heads_per_cta);
+        const int bl = l * a.block;
+        if (kq >= 1) mbar_wait(&q_empty, (kq - 1) & 1);  // every S of the previous plan done
+        mbar_expect_tx(&q_full, SM::Q);
+        for (int rg = 0; rg < 2 * MT; ++rg) {
+          const int h = qh0 + (rg < nh ? rg : 0);
+          const int row = h * a.L + bl;
+          for (int half = 0; half < 2; ++half)
+            tma_load_2d(smem + SM::q_off + (rg >> 1) * 32768 + half * 16384 + (rg & 1) * 8192, &tmQ,
+                        &q_full, half * 64, row);
+        }
+        for (int j = 0; j < np; ++j, ++jg) {
+          const int st = jg % NST;
+          if (jg >= NST) mbar_wait(&kv_empty[st], ((jg / NST) - 1) & 1);
+          mbar_expect_tx(&kv_full[st], SM::KV);
+          const int row = unit * a.L + s_plan[b][j].x;
+          unsigned char* kb = smem + SM::kv_off + st * SM::KV;
+          for (int half = 0; half < 2; ++half) {
+            tma_load_2d(kb + half * 8192, &tmK, &kv_full[st], half * 64, row);
+            tma_load_2d(kb + 16384 + half * 8192, &tmV, &kv_full[st], half * 64, row);
+          }
+        }
+      }
+      jg = __shfl_sync(0xffffffffu, jg, 0);
+      ++kq;
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer (one thread)
+    if (lane == 0) {
+      constexpr uint32_t idS = umma_idesc_bf16(128, 64, 0, 0);
+      constexpr uint32_t idO = umma_idesc_bf16(128, 128, 0, 1);
+      int jg0 = 0, kq = 0;
+      for (int k = 0;; ++k) {
+        const int b = k & 1;
+        mbar_wait(&plan_full[b], (k >> 1) & 1);
+        const int4 m = s_meta[b];
+        if (m.x < 0) break;
+        const int np = m.y;
+        if (np <= 0) {
+          mbar_arrive(&plan_empty[b]);
+          continue;
+        }
+        mbar_wait(&q_full, kq & 1);
+        auto issue_s = [&](int jj) {
+          const int st = jj % NST;
+          mbar_wait(&kv_full[st], (jj / NST) & 1);
+          tc_fence_after();
+          const uint32_t kb = skv + st * SM::KV;
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk) {
+              const uint64_t ad = umma_sdesc(sq + mt * 32768 + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
+              const uint64_t bd = umma_sdesc(kb + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024);
+              umma_bf16(tmem + mt * 256 + (jj & 1) * 64, ad, bd, idS, kk > 0);
+            }
+          }
+          umma_commit(&s_full[jj & 1]);
+        };
+        issue_s(jg0);
+        if (np == 1) umma_commit(&q_empty);
+        for (int j = 0; j < np; ++j) {
+          const int jj = jg0 + j;
+          if (j + 1 < np) {
+            issue_s(jj + 1);
+            if (j + 2 == np) umma_commit(&q_empty);  // the plan's last S: Q may be replaced
+          }
+          mbar_wait(&p_full[jj & 1], (jj >> 1) & 1);
+          if (j == 0 && kq >= 1) mbar_wait(&o_free, (kq - 1) & 1);  // O of the previous plan read
+          tc_fence_after();
+          const int st = jj % NST;
+          const uint32_t vb = skv + st * SM::KV + 16384;
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint64_t bd = umma_sdesc(vb + kk * 2048, 8192, 1024);
+              umma_bf16_ts(tmem + mt * 256 + 128, tmem + mt * 256 + (jj & 1) * 64 + kk * 8, bd, idO,
+                           (j > 0 || kk > 0) ? 1u : 0u);
+            }
+          }
+          umma_commit(&kv_empty[st]);
+          umma_commit(&o_done[jj & 1]);
+        }
+        mbar_arrive(&plan_empty[b]);
+        jg0 += np;
+        ++kq;
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------ softmax / epilogue warps
+    const int sw = warp - 2;
+    const int mt = sw >> 2;
+    const int quad = warp & 3;
+    const int trow = quad * 32 + lane;
+    const int r = mt * 128 + trow;
+    const int rg = r >> 6;
+    const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
+    const uint32_t tS = tmem + lane_base + mt * 256;
+    const uint32_t tO = tS + 128;
+    const float sl2 = a.scale_log2;
+    int jg0 = 0;
+    for (int k = 0;; ++k) {
+      const int b = k & 1;
+      mbar_wait(&plan_full[b], (k >> 1) & 1);
+      const int4 m = s_meta[b];
+      if (m.x < 0) break;
+      const int np = m.y;
+      if (np <= 0) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&plan_empty[b]);
+        continue;
+      }
+      const int l = m.z, sr = m.w / a.slices, hs = m.w - sr * a.slices;
+      const int qh0 = (a.per_head ? sr : sr * a.G) + hs * a.heads_per_cta;
+      const int nh = a.per_head ? 1 : min(a.heads_per_cta, a.G - hs * a.heads_per_cta);
+      const int bl = l * a.block;
+      const int i = bl + (r & 63);
+      const bool live = rg < nh && i < a.L;
+      const int64_t keep = a.budget < (int64_t)i + 1 ? a.budget : (int64_t)i + 1;
+      const int Ri = (int)(keep - 1);
+      const int dl = i - bl;
+      float m_used = -INFINITY, lsum = 0.f;
+      for (int j = 0; j < np; ++j) {
+        const int jj = jg0 + j;
+        const int4 e = s_plan[b][j];
+        int lim, self = -1;
+        if (e.w & 2) {
+          lim = max(0, min(Ri - e.z, dl));
+          self = dl;
+        } else {
+          lim = max(0, min(Ri - e.z - ((e.w & 1) ? dl : 0), e.y));
+        }
+        if (!live) {
+          lim = 0;
+          self = -1;
+        }
+        mbar_wait(&s_full[jj & 1], (jj >> 1) & 1);
+        tc_fence_after();
+        uint32_t v[64];
+        tmem_ld32(tS + (jj & 1) * 64, *reinterpret_cast<uint32_t(*)[32]>(v));
+        tmem_ld32(tS + (jj & 1) * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+        tmem_wait_ld();
+        float mx = -INFINITY;
+        if (__all_sync(0xffffffffu, lim == 64 && self < 0)) {
+#pragma unroll
+          for (int c = 0; c < 64; ++c) mx = fmaxf(mx, __uint_as_float(v[c]));
+        } else {
+#pragma unroll
+          for (int c = 0; c < 64; ++c) {
+            if (!(c < lim || c == self)) v[c] = __float_as_uint(-INFINITY);
+            mx = fmaxf(mx, __uint_as_float(v[c]));
+          }
+        }
+        mx *= sl2;
+        float m_new = m_used;
+        if (mx > -INFINITY && (m_used == -INFINITY || mx > m_used + 8.f)) m_new = mx;
+        const bool need = m_used != -INFINITY && m_new != m_used;
+        if (__any_sync(0xffffffffu, need)) {
+          mbar_wait(&o_done[(jj - 1) & 1], ((jj - 1) >> 1) & 1);  // j >= 1 here
+          tc_fence_after();
+          const float f = need ? exp2f(m_used - m_new) : 1.f;
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            uint32_t o[32];
+            tmem_ld32(tO + cc * 32, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int t = 0; t < 32; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * f);
+            tmem_st32(tO + cc * 32, o);
+          }
+          tmem_wait_st();
+          lsum *= f;
+        }
+        m_used = m_new;
+        const float mref = m_used == -INFINITY ? 0.f : m_used;
+        uint32_t pk[32];
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+          const float p0 = exp2_mufu(fmaf(__uint_as_float(v[2 * t]), sl2, -mref));
+          const float p1 = exp2_mufu(fmaf(__uint_as_float(v[2 * t + 1]), sl2, -mref));
+          lsum += p0 + p1;
+          pk[t] = pack_bf16(p0, p1);
+        }
+        tmem_st32(tS + (jj & 1) * 64, pk);
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[jj & 1]);
+      }
+      const int jl = jg0 + np - 1;
+      mbar_wait(&o_done[jl & 1], (jl >> 1) & 1);  // in-order: every PV of the plan done
+      tc_fence_after();
+      const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
+      __nv_bfloat16* orow = a.out + ((int64_t)(qh0 + (rg < nh ? rg : 0)) * a.L + i) * D;
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        uint32_t o[32];
+        tmem_ld32(tO + cc * 32, o);
+        tmem_wait_ld();
+        if (live) {
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            uint4 pk4;
+            pk4.x = pack_bf16(__uint_as_float(o[8 * t + 0]) * inv, __uint_as_float(o[8 * t + 1]) * inv);
+            pk4.y = pack_bf16(__uint_as_float(o[8 * t + 2]) * inv, __uint_as_float(o[8 * t + 3]) * inv);
+            pk4.z = pack_bf16(__uint_as_float(o[8 * t + 4]) * inv, __uint_as_float(o[8 * t + 5]) * inv);
+            pk4.w = pack_bf16(__uint_as_float(o[8 * t + 6]) * inv, __uint_as_float(o[8 * t + 7]) * inv);
+            *reinterpret_cast<uint4*>(orow + cc * 32 + 8 * t) = pk4;
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&o_free);         // the next plan's first PV may overwrite O
+        mbar_arrive(&plan_empty[b]);  // plan entries no longer read
+      }
+      jg0 += np;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, kTmemCols);
+  }
+  if (threadIdx.x == 0) {  // the last CTA out re-arms the plan counter
+    __threadfence();
+    if (atomicAdd(a.counters + 1, 1) == (int)gridDim.x - 1) {
+      a.counters[0] = 0;
+      a.counters[1] = 0;
+    }
+  }
+}
+
+template <int MT, int NST>
+static int launch_prefill_persist(const CUtensorMap& mq, const CUtensorMap& mk,
+                                  const CUtensorMap& mv, const PrefillArgs& a, cudaStream_t st) {
+  using SM = PrefillSmem<MT, NST>;
+  auto kern = prefill_attn_persist_kernel<MT, NST>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::total);
+  if (e != cudaSuccess) {
+    set_error("dhsa_prefill_attn: %s", cudaGetErrorString(e));
+    return DHSA_ECUDA;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int total = a.S * a.nc * a.slices;
+  const int grid = total < sms ? total : sms;
+  kern<<<grid, 64 + 128 * MT, SM::total, st>>>(mq, mk, mv, a);
+  return check_launch("dhsa_prefill_attn");
+}
+
 template <int MT, int NST>
 static int launch_prefill_attn(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
                                const PrefillArgs& a, int S, cudaStream_t st) {
@@ -543,7 +895,7 @@ extern "C" int dhsa_prefill_plan(const double* scores, int S, int n_chunks, int 
 
 extern "C" int dhsa_prefill_attn(const void* q, const void* k, const void* v, int U, int G, int L,
                                  int D, int block, int agg, int64_t budget, const void* plans,
-                                 const int32_t* nplan, int cap, void* out,
+                                 const int32_t* nplan, int cap, void* out, int32_t* counters,
                                  dhsa_stream_t stream) {
   DHSA_REQUIRE(q && k && v && plans && nplan && out, "dhsa_prefill_attn: null pointer");
   DHSA_REQUIRE(D == 128, "dhsa_prefill_attn: head_dim must be 128 (got %d)", D);
@@ -579,7 +931,17 @@ extern "C" int dhsa_prefill_attn(const void* q, const void* k, const void* v, in
   a.out = (__nv_bfloat16*)out;
   a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)D));
   const int S = per_head ? U * G : U;
+  a.S = S;
+  a.counters = counters;
   cudaStream_t st = (cudaStream_t)stream;
+  // persistent plans pay off when plans are short (per-plan start-up is a
+  // large share): measured +7% at budget 1025, -3..-9% at 4097..16385
+  bool persist = counters != nullptr && budget <= 1600;
+  if (const char* e = getenv("DHSA_PREFILL_PERSISTENT")) persist = counters != nullptr && atoi(e) != 0;
+  if (persist) {
+    if (a.heads_per_cta > 2) return launch_prefill_persist<2, 4>(mq, mk, mv, a, st);
+    return launch_prefill_persist<1, 5>(mq, mk, mv, a, st);
+  }
   if (a.heads_per_cta > 2) return launch_prefill_attn<2, 4>(mq, mk, mv, a, S, st);
   return launch_prefill_attn<1, 5>(mq, mk, mv, a, S, st);
 }

@@ -15,7 +15,8 @@ L x L upsampled score matrix:
   3. ``dhsa_prefill_plan``    per (selection row, query chunk) the walk-order
                               list of selected chunks (SURVEY Appendix A);
   4. ``dhsa_prefill_attn``    tcgen05.mma S = Q K^T / O += P V over the planned
-                              64-token KV blocks, per-row masks, online softmax.
+                              64-token KV blocks, per-row masks, online softmax
+                              (a persistent plan-pulling grid for short plans).
 
 Layouts (dense, bf16): q [B, Hq, L, D], k/v [B, Hkv, L, D], out [B, Hq, L, D].
 Static 64-token chunks (chunking.static_boundaries) and D = 128.
@@ -68,6 +69,7 @@ class SparsePrefill:
         self.nplan = torch.zeros(self.S, self.nc, dtype=torch.int32, **kw)
         self.plen_q = torch.full((self.U * self.G,), seq_len, dtype=torch.int32, **kw)
         self.plen_k = torch.full((self.U,), seq_len, dtype=torch.int32, **kw)
+        self.counters = torch.zeros(2, dtype=torch.int32, **kw)  # persistent attention
 
     def _check(self, q, k, v):
         want_q = (self.B, self.Hq, self.L, self.D)
@@ -101,7 +103,8 @@ class SparsePrefill:
         def attn():
             _lib.call("dhsa_prefill_attn", _lib.ptr(q), _lib.ptr(k), _lib.ptr(v), self.U, self.G,
                       self.L, self.D, self.block, _lib.AGG[self.agg], self.budget,
-                      _lib.ptr(self.plans), _lib.ptr(self.nplan), self.cap, _lib.ptr(out), st)
+                      _lib.ptr(self.plans), _lib.ptr(self.nplan), self.cap, _lib.ptr(out),
+                      _lib.ptr(self.counters), st)
 
         return [("chunk_reps", reps), ("chunk_scores", scores), ("plan", plan), ("attn", attn)]
 

@@ -122,3 +122,13 @@ def test_prefill_tiny_lengths(L):
     """A single (short) chunk, exactly one block, one block + 1 token."""
     worst = _run(B=1, Hq=4, Hkv=1, L=L, top_k=1, agg="max", seed=60 + L, check_rows=range(L))
     assert worst <= TOL_BF16, worst
+
+
+@pytest.mark.parametrize("persistent", ["0", "1"])
+def test_prefill_both_grids(persistent, monkeypatch):
+    """The persistent plan-pulling grid and the one-CTA-per-plan grid give the
+    same (exact) selections and in-tolerance outputs."""
+    monkeypatch.setenv("DHSA_PREFILL_PERSISTENT", persistent)
+    worst = _run(B=2, Hq=8, Hkv=2, L=1536, top_k=6, agg="max", seed=77,
+                 check_rows=range(0, 1536, 11))
+    assert worst <= TOL_BF16, worst
