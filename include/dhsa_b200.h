@@ -326,6 +326,13 @@ int dhsa_prefill_plan(const double* scores, int S, int n_chunks, int L, int bloc
                       int64_t budget, int cap, void* plans, int32_t* nplan,
                       dhsa_stream_t stream);
 
+/* The token sets the plans encode as DHSAMSK1 row bitsets (the reference's
+ * mask file payload, serialization.py:80-94): out [S][L][ceil(L/8)] bytes,
+ * token t of row i = bit t % 8 of byte t / 8 (self included). */
+int dhsa_prefill_mask_bitsets(const void* plans, const int32_t* nplan, int cap, int S,
+                              int n_chunks, int L, int block, int64_t budget, uint8_t* out,
+                              dhsa_stream_t stream);
+
 /* Block-sparse attention of every query row over its planned tokens:
  * softmax(K[idx] q / sqrt(D)) @ V[idx] (core.py:113-118) with tcgen05.mma
  * (bf16 operands from TMA-staged 128B-swizzled shared memory, fp32 TMEM

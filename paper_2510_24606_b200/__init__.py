@@ -13,6 +13,7 @@ from .chunking import check_boundaries, extend_for_decode, nms_boundaries, stati
 from .core import TokenSequence, dense_attention
 from .chunk_repr import ChunkReps, aggregate_chunk, aggregate_rows, build_chunk_reps, \
     chunk_similarity
+from . import serialization
 from .masks import CostCounters, DecodeSession, SparsityMask, decode_mask_row, \
     mask_from_chunk_scores, prefill_mask, topk_row, upsample
 

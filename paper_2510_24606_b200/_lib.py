@@ -77,6 +77,8 @@ _SIGS = {
     "dhsa_prefill_scores": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp,
                                       vp]),
     "dhsa_prefill_plan_capacity": (C.c_int, [C.c_int64, C.c_int]),
+    "dhsa_prefill_mask_bitsets": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                            C.c_int64, vp, vp]),
     "dhsa_prefill_plan": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int,
                                     vp, vp, vp]),
     "dhsa_prefill_attn": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,

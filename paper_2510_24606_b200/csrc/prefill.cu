@@ -842,9 +842,74 @@ static int launch_prefill_attn(const CUtensorMap& mq, const CUtensorMap& mk, con
   return check_launch("dhsa_prefill_attn");
 }
 
+// ----------------------------------------------------- mask export (8f) --
+// The per-row token sets the plans encode, as the reference's DHSAMSK1 row
+// bitsets (serialization.py:80-94: ceil(L/8) bytes per row, token t = bit
+// t % 8 of byte t / 8).  One CTA per (query chunk, selection row); each row
+// is assembled in shared memory with word atomics and streamed out.
+__global__ __launch_bounds__(128) void plan_bitsets_kernel(const int4* __restrict__ plans,
+                                                           const int32_t* __restrict__ nplan,
+                                                           int cap, int nc, int L, int block,
+                                                           int64_t budget, int64_t nbytes,
+                                                           uint8_t* __restrict__ out) {
+  extern __shared__ uint32_t rowbits[];
+  const int l = blockIdx.x, s = blockIdx.y, tid = threadIdx.x;
+  const int np = nplan[(int64_t)s * nc + l];
+  const int4* plan = plans + ((int64_t)s * nc + l) * cap;
+  const int nwords = (int)((nbytes + 3) / 4);
+  const int bl = l * block, el = min(bl + block, L);
+  for (int i = bl; i < el; ++i) {
+    for (int w = tid; w < nwords; w += 128) rowbits[w] = 0u;
+    __syncthreads();
+    const int64_t keep = budget < (int64_t)i + 1 ? budget : (int64_t)i + 1;
+    const int Ri = (int)(keep - 1), dl = i - bl;
+    for (int e = tid; e < np; e += 128) {
+      const int4 en = plan[e];
+      const int lim = (en.w & 2) ? max(0, min(Ri - en.z, dl))
+                                 : max(0, min(Ri - en.z - ((en.w & 1) ? dl : 0), en.y));
+      for (int t = en.x; t < en.x + lim;) {  // word-sized pieces of [start, start + lim)
+        const int w = t >> 5, b0 = t & 31;
+        const int n = min(32 - b0, en.x + lim - t);
+        const uint32_t m = (n == 32 ? 0xFFFFFFFFu : ((1u << n) - 1u)) << b0;
+        atomicOr(&rowbits[w], m);
+        t += n;
+      }
+    }
+    if (tid == 0 && np > 0) atomicOr(&rowbits[i >> 5], 1u << (i & 31));  // self
+    __syncthreads();
+    uint8_t* dst = out + ((int64_t)s * L + i) * nbytes;
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(rowbits);  // little-endian words
+    for (int64_t b = tid; b < nbytes; b += 128) dst[b] = src[b];
+    __syncthreads();
+  }
+}
+
 }  // namespace dhsa
 
 using namespace dhsa;
+
+extern "C" int dhsa_prefill_mask_bitsets(const void* plans, const int32_t* nplan, int cap, int S,
+                                         int n_chunks, int L, int block, int64_t budget,
+                                         uint8_t* out, dhsa_stream_t stream) {
+  DHSA_REQUIRE(plans && nplan && out && S >= 1 && n_chunks >= 1 && L >= 1 && block >= 1,
+               "dhsa_prefill_mask_bitsets: bad arguments");
+  DHSA_REQUIRE(budget >= 1, "budget must be >= 1");
+  const int64_t nbytes = ((int64_t)L + 7) / 8;
+  const size_t smem = (size_t)((nbytes + 3) / 4) * 4;
+  DHSA_REQUIRE(smem <= 200 * 1024, "dhsa_prefill_mask_bitsets: L too large (%d)", L);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(plan_bitsets_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) {
+      set_error("dhsa_prefill_mask_bitsets: %s", cudaGetErrorString(e));
+      return DHSA_ECUDA;
+    }
+  }
+  dim3 grid((unsigned)n_chunks, (unsigned)S);
+  plan_bitsets_kernel<<<grid, 128, smem, (cudaStream_t)stream>>>(
+      (const int4*)plans, nplan, cap, n_chunks, L, block, budget, nbytes, out);
+  return check_launch("dhsa_prefill_mask_bitsets");
+}
 
 extern "C" int dhsa_prefill_scores(const double* q_centroids, const double* k_centroids, int U,
                                    int G, int n_chunks, int D, int agg, double* scores,

@@ -116,6 +116,18 @@ class SparsePrefill:
             fn()
         return out
 
+    def mask_bitsets(self, stream=None):
+        """The last call's per-row selections as DHSAMSK1 bitsets
+        [S, L, ceil(L/8)] uint8 on the device (selection row s = kv unit, or
+        q head with agg "none"); ``serialization.save_mask_bitsets`` writes
+        one selection row as the reference's mask file."""
+        nbytes = (self.L + 7) // 8
+        out = torch.empty(self.S, self.L, nbytes, dtype=torch.uint8, device=self.dev)
+        _lib.call("dhsa_prefill_mask_bitsets", _lib.ptr(self.plans), _lib.ptr(self.nplan),
+                  self.cap, self.S, self.nc, self.L, self.block, self.budget, _lib.ptr(out),
+                  _lib.stream_handle(stream))
+        return out
+
     def check_capacity(self):
         if int(self.nplan.min().item()) < 0:
             raise _lib.DhsaError("prefill plan capacity exceeded")

@@ -18,6 +18,8 @@ group.npz     group-shared decode rows: mask_from_chunk_scores over the
               head-aggregated S_c (harness.py:288-306) on extend_for_decode
               bounds, agg = max and mean, 4 heads sharing one key set (GQA)
 centroids.npz aggregate_rows (chunk_repr.py:57-68), bitwise
+wire_*        DHSAMSK1 / DHSATEN1 / JSON files written by the reference's
+              serialization.py (a prefill mask, a tensor) for byte-level parity
 nms.npz       nms_boundaries (chunking.py:57-89) on 300 random score vectors
               incl. forced ties, with random min_conf / window / max_chunks
 c1.npz        the C1 demo shape (L=4096, 8 heads, d=64, block 64, top-k 16,
@@ -216,6 +218,24 @@ def gen_nms():
                         params=np.array(params, dtype=np.float64), bounds=ov, bounds_off=oo)
 
 
+def gen_wire():
+    from dhsa.serialization import mask_to_json, save_mask, save_tensor
+
+    rng = np.random.default_rng(21)
+    L, d = 300, 16
+    seq = TokenSequence(rng.standard_normal((L, d)), rng.standard_normal((L, d)),
+                        rng.standard_normal((L, d)))
+    mask = prefill_mask(seq, static_boundaries(L, 64), 100)
+    save_mask(os.path.join(OUT, "wire_mask.msk"), mask)
+    with open(os.path.join(OUT, "wire_mask.json"), "w") as fh:
+        fh.write(mask_to_json(mask))
+    flat, off = pack_rows(mask.rows)
+    np.savez_compressed(os.path.join(OUT, "wire_rows.npz"), rows=flat, off=off, length=L)
+    t = rng.standard_normal((7, 5)).astype(np.float32)
+    save_tensor(os.path.join(OUT, "wire_tensor.ten"), t)
+    np.save(os.path.join(OUT, "wire_tensor.npy"), t)
+
+
 def c1_inputs(seed=7):
     """C1 demo shape; regenerated identically by tests (numpy PCG64)."""
     rng = np.random.default_rng(seed)
@@ -272,4 +292,5 @@ if __name__ == "__main__":
     gen_centroids()
     gen_c1()
     gen_nms()
+    gen_wire()
     print("golden fixtures written to", OUT)

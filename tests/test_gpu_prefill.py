@@ -132,3 +132,27 @@ def test_prefill_both_grids(persistent, monkeypatch):
     worst = _run(B=2, Hq=8, Hkv=2, L=1536, top_k=6, agg="max", seed=77,
                  check_rows=range(0, 1536, 11))
     assert worst <= TOL_BF16, worst
+
+
+def test_prefill_mask_export_matches_reference_format(tmp_path):
+    """GPU plan -> DHSAMSK1 bitsets: the file written from the device bitsets
+    equals the file of the oracle's rows (the reference's format)."""
+    from paper_2510_24606_b200 import serialization as S
+    from paper_2510_24606_b200.prefill import SparsePrefill
+
+    L, D = 700, 128
+    t, host = _inputs(1, 4, 1, L, D, 81)
+    pf = SparsePrefill(1, 4, 1, D, L, budget=150, agg="max")
+    pf(t["q"].cuda(), t["k"].cuda(), t["v"].cuda())
+    bits = pf.mask_bitsets()
+    S.save_mask_bitsets(tmp_path / "gpu.msk", L, bits[0])
+    rows = O.prefill_rows(host["q"][0], np.repeat(host["k"][0, 0][None], 4, axis=0),
+                          O.static_grid(L, 64), pf.budget)
+
+    class M:
+        length = L
+
+    m = M()
+    m.rows = rows
+    S.save_mask(tmp_path / "oracle.msk", m)
+    assert (tmp_path / "gpu.msk").read_bytes() == (tmp_path / "oracle.msk").read_bytes()

@@ -218,3 +218,32 @@ def test_c_abi_new_entry_points_exported():
     lib.dhsa_prefill_plan_capacity.argtypes = [ctypes.c_int64, ctypes.c_int]
     assert lib.dhsa_prefill_plan_capacity(4097, 64) == 66
     assert lib.dhsa_prefill_plan_capacity(0, 64) == -1
+
+
+def test_wire_formats_byte_identical(tmp_path):
+    """DHSAMSK1 / DHSATEN1 / JSON mask files byte-identical to the ones the
+    reference's serialization.py wrote (tests/golden/wire_*), and round trips."""
+    import golden_io as GI
+    from paper_2510_24606_b200 import serialization as S
+
+    z = GI.load("wire_rows.npz")
+    rows = GI.unpack_rows(z["rows"], z["off"])
+    mask = P.SparsityMask(length=int(z["length"]), rows=tuple(rows))
+    S.save_mask(tmp_path / "m.msk", mask)
+    ref = open(os.path.join(GI.GOLDEN, "wire_mask.msk"), "rb").read()
+    assert (tmp_path / "m.msk").read_bytes() == ref
+    n, back = S.load_mask(os.path.join(GI.GOLDEN, "wire_mask.msk"))
+    assert n == mask.length and all(np.array_equal(a, b) for a, b in zip(back, rows))
+    assert S.mask_to_json(mask) == open(os.path.join(GI.GOLDEN, "wire_mask.json")).read()
+    n2, rows2 = S.mask_from_json(S.mask_to_json(mask))
+    assert n2 == mask.length and all(np.array_equal(a, b) for a, b in zip(rows2, rows))
+    t = np.load(os.path.join(GI.GOLDEN, "wire_tensor.npy"))
+    S.save_tensor(tmp_path / "t.ten", t)
+    assert (tmp_path / "t.ten").read_bytes() == open(os.path.join(GI.GOLDEN, "wire_tensor.ten"),
+                                                     "rb").read()
+    assert np.array_equal(S.load_tensor(tmp_path / "t.ten"), t.astype(np.float64))
+    with pytest.raises(ValueError):
+        S.save_tensor(tmp_path / "x.ten", np.zeros(3))
+    (tmp_path / "bad.msk").write_bytes(b"NOTAMASK")
+    with pytest.raises(ValueError):
+        S.load_mask(tmp_path / "bad.msk")
