@@ -540,6 +540,29 @@ def run_gpu_c5(args):
                           "attn_frac_of_peak": fl / (attn_ms * 1e-3) / 1e12 / peak,
                           "prefill_tokens_per_s": B * L / (ms * 1e-3)})
     head = next((x for x in sweep if x["top_k"] == 64), sweep[0])
+    # mask quality at 32K: recall / output fidelity of the
+    # top-k masks against dense causal attention, both on the tcgen05 kernel
+    from paper_2510_24606_b200.prefill import mask_quality
+
+    quality = None
+    if not args.no_quality:
+        pf = SparsePrefill(B, Hq, Hkv, D, L, top_k=head["top_k"], agg="max")
+        rec, cos = mask_quality(q, k, v, pf)
+        dense = SparsePrefill(B, Hq, Hkv, D, L, budget=L + 1, agg="max")
+        dense(q, k, v, out)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        flush.zero_()
+        e0.record()
+        dense(q, k, v, out)
+        e1.record()
+        torch.cuda.synchronize()
+        dms = e0.elapsed_time(e1)
+        quality = {"top_k": head["top_k"], "attention_mass_recall": float(rec.mean()),
+                   "output_fidelity": float(cos.mean()),
+                   "dense_causal_ms": dms, "dense_causal_tflops": dense.flops() / (dms * 1e-3) / 1e12,
+                   "note": "harness.attention_mass_recall / output_fidelity semantics over all "
+                           "32 heads and 32K rows (the CPU harness needs the 8.6 GB L x L matrix)"}
     result = {
         "metric": "sparse prefill ms per 32K-token sequence (C5); tensor TFLOP/s vs roofline",
         "value": head["ms"], "unit": "ms", "n_gpus": world, "steps": S, "warmup": W,
@@ -553,7 +576,7 @@ def run_gpu_c5(args):
                      "peak": peak, "unit": "TFLOP/s", "frac": head["attn_frac_of_peak"],
                      "peak_source": "measured (MEASURED_PEAKS.json bf16_tflops)" if tf_peak
                      else "fallback (B200_PROFILING.md)", "peak_sustained": tf_sust},
-        "sweep": sweep, "gpu_launches": 5 * S, "clocks": clk.summary(),
+        "sweep": sweep, "mask_quality": quality, "gpu_launches": 5 * S, "clocks": clk.summary(),
     }
     if rank == 0:
         print(json.dumps(result), flush=True)
@@ -607,6 +630,7 @@ def main():
     ap.add_argument("--splits", type=int, default=None)
     ap.add_argument("--cpu-units", type=int, default=None)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-quality", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     # the reference arm: every "step" is one bounded CPU sample (~0.6 s)

@@ -339,11 +339,21 @@ int dhsa_prefill_mask_bitsets(const void* plans, const int32_t* nplan, int cap, 
  * accumulators, P kept in TMEM), per (plan, <= 4 q heads).  out [U*G][L][D]
  * bf16.  counters: int32[2] zero at rest -> persistent grid (one CTA per SM
  * pulling plans, TMEM / barriers / K-V ring kept across plans); NULL -> one
- * CTA per (plan, head slice). */
+ * CTA per (plan, head slice).  row_stats (float2 [U*G][L], or NULL): per
+ * query row the softmax reference max m (log2 domain) and l = sum over the
+ * selection of 2^(x - m), x = q.k log2(e) / sqrt(D). */
 int dhsa_prefill_attn(const void* q, const void* k, const void* v, int U, int G, int L, int D,
                       int block, int agg, int64_t budget, const void* plans,
                       const int32_t* nplan, int cap, void* out, int32_t* counters,
-                      dhsa_stream_t stream);
+                      float* row_stats, dhsa_stream_t stream);
+
+/* Mask quality per query row (harness.attention_mass_recall / output_fidelity,
+ * harness.py:265-285) from a sparse and a dense (budget >= L) prefill run:
+ * recall = l_sel 2^(m_sel - m_all) / l_all, cosine(o_sel, o_all).
+ * stats_*: float2 [rows] from dhsa_prefill_attn; out_*: bf16 [rows][D]. */
+int dhsa_row_quality(const float* stats_sel, const float* stats_all, const void* out_sel,
+                     const void* out_all, int64_t rows, int D, float* recall, float* cosine,
+                     dhsa_stream_t stream);
 
 /* f_upsample (masks.upsample, masks.py:87-100): out[i][j] = s[chunk(i)][chunk(j)]
  * for an n x n chunk-score matrix and bounds [n+1]; out is L x L fp64.  Only

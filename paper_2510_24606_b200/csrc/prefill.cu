@@ -188,6 +188,8 @@ __global__ __launch_bounds__(kPlanThreads) void prefill_plan_kernel(
 }
 
 // ------------------------------------------------------------------- K9 --
+constexpr int kPlanCap = 544;  // plan entries per query chunk (dense up to ~34K tokens)
+
 struct PrefillArgs {
   const int4* plans;
   const int32_t* nplan;
@@ -198,6 +200,8 @@ struct PrefillArgs {
   float scale_log2;
   int S;               // selection rows
   int32_t* counters;   // [2] plan pull counter, exits (persistent kernel); zero at rest
+  float2* row_stats;   // [q heads][L] (m, l): the row's softmax reference max (log2
+                       // domain) and sum of 2^(x - m) over its selection, or null
 };
 
 template <int MT, int NST>
@@ -250,7 +254,7 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_kernel(
   __shared__ __align__(8) uint64_t kv_full[NST], kv_empty[NST], s_full[2], p_full[2], o_done[2],
       q_full;
   __shared__ uint32_t s_tmem;
-  __shared__ int4 s_plan[288];
+  __shared__ int4 s_plan[kPlanCap];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int hs = blockIdx.x;                   // head slice of the selection row
@@ -263,7 +267,7 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_kernel(
   const int np = __ldg(a.nplan + (int64_t)s * a.nc + l);
   const int4* plan = a.plans + ((int64_t)s * a.nc + l) * a.cap;
   if (np <= 0) return;  // capacity overflow (nplan = -1): reported by the host
-  for (int e = threadIdx.x; e < np && e < 288; e += blockDim.x) s_plan[e] = plan[e];
+  for (int e = threadIdx.x; e < np && e < kPlanCap; e += blockDim.x) s_plan[e] = plan[e];
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NST; ++i) {
@@ -452,6 +456,7 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_kernel(
     mbar_wait(&o_done[(np - 1) & 1], ((np - 1) >> 1) & 1);  // in-order: every PV done
     tc_fence_after();
     const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
+    if (a.row_stats && live) a.row_stats[(int64_t)(qh0 + rg) * a.L + i] = make_float2(m_used, lsum);
     __nv_bfloat16* orow = a.out + ((int64_t)(qh0 + (rg < nh ? rg : 0)) * a.L + i) * D;
 #pragma unroll
     for (int cc = 0; cc < 4; ++cc) {
@@ -499,7 +504,7 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_persist_kernel(
   __shared__ __align__(8) uint64_t kv_full[NST], kv_empty[NST], s_full[2], p_full[2], o_done[2],
       q_full, q_empty, o_free, plan_full[2], plan_empty[2];
   __shared__ uint32_t s_tmem;
-  __shared__ int4 s_plan[2][288];
+  __shared__ int4 s_plan[2][kPlanCap];
   __shared__ int4 s_meta[2];  // (plan id or -1, entries, l, s * slices + hs)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -563,7 +568,7 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_persist_kernel(
       decode(p, l, sr, hs);
       const int np = __ldg(a.nplan + (int64_t)sr * a.nc + l);
       const int4* plan = a.plans + ((int64_t)sr * a.nc + l) * a.cap;
-      for (int e = lane; e < np && e < 288; e += 32) s_plan[b][e] = __ldg(plan + e);
+      for (int e = lane; e < np && e < kPlanCap; e += 32) s_plan[b][e] = __ldg(plan + e);
       if (lane == 0) s_meta[b] = make_int4(p, np, l, sr * a.slices + hs);
       __syncwarp();
       if (lane == 0) mbar_arrive(&plan_full[b]);
@@ -766,6 +771,7 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_persist_kernel(
       mbar_wait(&o_done[jl & 1], (jl >> 1) & 1);  // in-order: every PV of the plan done
       tc_fence_after();
       const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
+      if (a.row_stats && live) a.row_stats[(int64_t)(qh0 + rg) * a.L + i] = make_float2(m_used, lsum);
       __nv_bfloat16* orow = a.out + ((int64_t)(qh0 + (rg < nh ? rg : 0)) * a.L + i) * D;
 #pragma unroll
       for (int cc = 0; cc < 4; ++cc) {
@@ -884,9 +890,53 @@ __global__ __launch_bounds__(128) void plan_bitsets_kernel(const int4* __restric
   }
 }
 
+// --------------------------------------------- mask quality (8f row 3) --
+// Per query row of one q head: the attention mass the selection captures,
+// sum_{j in sel} p_ij = l_sel 2^(m_sel - m_all) / l_all (harness.py:265-274,
+// from the sparse and the dense run's (m, l) row statistics), and the cosine
+// of the sparse and dense outputs (harness.py:277-285, core.py:139-152).
+// One warp per row.
+__global__ void row_quality_kernel(const float2* __restrict__ st_sel,
+                                   const float2* __restrict__ st_all,
+                                   const __nv_bfloat16* __restrict__ o_sel,
+                                   const __nv_bfloat16* __restrict__ o_all, int64_t rows, int D,
+                                   float* __restrict__ recall, float* __restrict__ cosine) {
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  double dot = 0.0, na = 0.0, nb = 0.0;
+  for (int d = lane; d < D; d += 32) {
+    const double x = __bfloat162float(o_sel[r * D + d]), y = __bfloat162float(o_all[r * D + d]);
+    dot += x * y;
+    na += x * x;
+    nb += y * y;
+  }
+  dot = warp_sum(dot);
+  na = warp_sum(na);
+  nb = warp_sum(nb);
+  if (lane == 0) {
+    const float2 s = st_sel[r], t = st_all[r];
+    recall[r] = t.y > 0.f ? (float)((double)s.y * exp2((double)s.x - (double)t.x) / (double)t.y) : 0.f;
+    cosine[r] = (na > 0.0 && nb > 0.0) ? (float)(dot / sqrt(na * nb)) : 0.f;
+  }
+}
+
 }  // namespace dhsa
 
 using namespace dhsa;
+
+extern "C" int dhsa_row_quality(const float* stats_sel, const float* stats_all,
+                                const void* out_sel, const void* out_all, int64_t rows, int D,
+                                float* recall, float* cosine, dhsa_stream_t stream) {
+  DHSA_REQUIRE(stats_sel && stats_all && out_sel && out_all && recall && cosine && rows >= 1 &&
+                   D >= 1,
+               "dhsa_row_quality: bad arguments");
+  const unsigned grid = (unsigned)((rows + 7) / 8);
+  row_quality_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
+      (const float2*)stats_sel, (const float2*)stats_all, (const __nv_bfloat16*)out_sel,
+      (const __nv_bfloat16*)out_all, rows, D, recall, cosine);
+  return check_launch("dhsa_row_quality");
+}
 
 extern "C" int dhsa_prefill_mask_bitsets(const void* plans, const int32_t* nplan, int cap, int S,
                                          int n_chunks, int L, int block, int64_t budget,
@@ -961,12 +1011,12 @@ extern "C" int dhsa_prefill_plan(const double* scores, int S, int n_chunks, int 
 extern "C" int dhsa_prefill_attn(const void* q, const void* k, const void* v, int U, int G, int L,
                                  int D, int block, int agg, int64_t budget, const void* plans,
                                  const int32_t* nplan, int cap, void* out, int32_t* counters,
-                                 dhsa_stream_t stream) {
+                                 float* row_stats, dhsa_stream_t stream) {
   DHSA_REQUIRE(q && k && v && plans && nplan && out, "dhsa_prefill_attn: null pointer");
   DHSA_REQUIRE(D == 128, "dhsa_prefill_attn: head_dim must be 128 (got %d)", D);
   DHSA_REQUIRE(block == 64, "dhsa_prefill_attn: the tcgen05 tiles need 64-token chunks");
-  DHSA_REQUIRE(U >= 1 && G >= 1 && L >= 1 && cap >= 2 && cap <= 288,
-               "dhsa_prefill_attn: bad shape (plan capacity <= 288)");
+  DHSA_REQUIRE(U >= 1 && G >= 1 && L >= 1 && cap >= 2 && cap <= kPlanCap,
+               "dhsa_prefill_attn: bad shape (plan capacity <= %d)", kPlanCap);
   DHSA_REQUIRE(budget >= 1, "budget must be >= 1");
   DHSA_REQUIRE(((uintptr_t)q & 15) == 0 && ((uintptr_t)k & 15) == 0 && ((uintptr_t)v & 15) == 0 &&
                    ((uintptr_t)out & 15) == 0,
@@ -998,6 +1048,7 @@ extern "C" int dhsa_prefill_attn(const void* q, const void* k, const void* v, in
   const int S = per_head ? U * G : U;
   a.S = S;
   a.counters = counters;
+  a.row_stats = reinterpret_cast<float2*>(row_stats);
   cudaStream_t st = (cudaStream_t)stream;
   // persistent plans pay off when plans are short (per-plan start-up is a
   // large share): measured +7% at budget 1025, -3..-9% at 4097..16385

@@ -57,8 +57,8 @@ class SparsePrefill:
         self.nc = (seq_len + block - 1) // block
         self.S = self.U * self.G if agg == "none" else self.U
         self.cap = _lib.load().dhsa_prefill_plan_capacity(self.budget, block)
-        if self.cap > 288:
-            raise ValueError("budget too large for the prefill plan (<= 286 blocks per row)")
+        if self.cap > 544:
+            raise ValueError("budget too large for the prefill plan (<= 542 blocks per row)")
         dev = torch.device(device) if device is not None else torch.device("cuda")
         self.dev = dev
         kw = dict(device=dev)
@@ -78,7 +78,7 @@ class SparsePrefill:
             if tuple(t.shape) != w or t.dtype != torch.bfloat16 or not t.is_contiguous():
                 raise ValueError(f"{n} must be a contiguous bf16 tensor of shape {w}")
 
-    def stages(self, q, k, v, out, stream=None):
+    def stages(self, q, k, v, out, stream=None, row_stats=None):
         """The launches as (name, thunk) pairs, in order."""
         st = _lib.stream_handle(stream)
         nq, nk = self.U * self.G, self.U
@@ -104,15 +104,17 @@ class SparsePrefill:
             _lib.call("dhsa_prefill_attn", _lib.ptr(q), _lib.ptr(k), _lib.ptr(v), self.U, self.G,
                       self.L, self.D, self.block, _lib.AGG[self.agg], self.budget,
                       _lib.ptr(self.plans), _lib.ptr(self.nplan), self.cap, _lib.ptr(out),
-                      _lib.ptr(self.counters), st)
+                      _lib.ptr(self.counters), _lib.ptr(row_stats), st)
 
         return [("chunk_reps", reps), ("chunk_scores", scores), ("plan", plan), ("attn", attn)]
 
-    def __call__(self, q, k, v, out=None, stream=None):
+    def __call__(self, q, k, v, out=None, stream=None, row_stats=None):
+        """Sparse prefill attention; ``row_stats`` (float32 [B, Hq, L, 2],
+        optional) receives each row's softmax (m, l) over its selection."""
         self._check(q, k, v)
         if out is None:
             out = torch.empty_like(q)
-        for _, fn in self.stages(q, k, v, out, stream):
+        for _, fn in self.stages(q, k, v, out, stream, row_stats):
             fn()
         return out
 
@@ -164,3 +166,29 @@ class SparsePrefill:
         m = min(L, b)
         tot = m * (m + 1) // 2 + (L - m) * b
         return 4.0 * tot * self.D * self.Hq * self.B
+
+
+def mask_quality(q, k, v, prefill: SparsePrefill, stream=None):
+    """Per-row quality of a sparse prefill's masks against dense causal
+    attention, on the GPU at any length (the reference computes them on the
+    full L x L probability matrix, harness.py:265-285):
+
+    * recall[b, h, i]  = fraction of row i's causal softmax mass inside its
+      selection (attention_mass_recall averages it over rows);
+    * cosine[b, h, i]  = cosine of the sparse and dense outputs of row i
+      (output_fidelity averages it).
+
+    The dense reference is the same tcgen05 kernel with a budget covering
+    every causal token.  Returns (recall, cosine) float32 [B, Hq, L]."""
+    B, Hq, L, D = q.shape
+    dense = SparsePrefill(B, Hq, prefill.Hkv, D, L, budget=L + 1, agg=prefill.agg, device=q.device)
+    kw = dict(dtype=torch.float32, device=q.device)
+    st_s = torch.empty(B, Hq, L, 2, **kw)
+    st_d = torch.empty(B, Hq, L, 2, **kw)
+    o_s = prefill(q, k, v, stream=stream, row_stats=st_s)
+    o_d = dense(q, k, v, stream=stream, row_stats=st_d)
+    recall = torch.empty(B, Hq, L, **kw)
+    cosine = torch.empty(B, Hq, L, **kw)
+    _lib.call("dhsa_row_quality", _lib.ptr(st_s), _lib.ptr(st_d), _lib.ptr(o_s), _lib.ptr(o_d),
+              B * Hq * L, D, _lib.ptr(recall), _lib.ptr(cosine), _lib.stream_handle(stream))
+    return recall, cosine
