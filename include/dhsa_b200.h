@@ -355,6 +355,18 @@ int dhsa_row_quality(const float* stats_sel, const float* stats_all, const void*
                      const void* out_all, int64_t rows, int D, float* recall, float* cosine,
                      dhsa_stream_t stream);
 
+/* Boundary-predictor inference (predictor.predict_sequence, predictor.py:
+ * 270-283 over _forward 198-207, _mha_pool_forward 101-117, _fuse_forward
+ * 151-161), fp64 like the reference.  keys [L][d]; wqkv [d][3d] = [Wq|Wk|Wv]
+ * column blocks; wo [d][d]; w1 [4d+1][hidden]; b1, w2 [hidden]; probs
+ * [L-2*window+1] = probabilities of positions window-1 .. L-window-1.
+ * Needs L >= 2*window+1, d % heads == 0, d/heads <= 32, window^2 <= 32. */
+int64_t dhsa_predictor_workspace_size(int L, int d, int window, int hidden);
+int dhsa_predictor_forward(const double* keys, int L, int d, int window, int heads, int hidden,
+                           const double* wqkv, const double* wo, const double* w1,
+                           const double* b1, const double* w2, double b2, void* workspace,
+                           double* probs, dhsa_stream_t stream);
+
 /* f_upsample (masks.upsample, masks.py:87-100): out[i][j] = s[chunk(i)][chunk(j)]
  * for an n x n chunk-score matrix and bounds [n+1]; out is L x L fp64.  Only
  * the drop-in API uses it — the selection kernels never materialise it. */

@@ -13,7 +13,7 @@ from .chunking import check_boundaries, extend_for_decode, nms_boundaries, stati
 from .core import TokenSequence, dense_attention
 from .chunk_repr import ChunkReps, aggregate_chunk, aggregate_rows, build_chunk_reps, \
     chunk_similarity
-from . import serialization
+from . import predictor, serialization
 from .masks import CostCounters, DecodeSession, SparsityMask, decode_mask_row, \
     mask_from_chunk_scores, prefill_mask, topk_row, upsample
 
@@ -25,7 +25,7 @@ __all__ = [
     "ChunkReps", "aggregate_chunk", "aggregate_rows", "build_chunk_reps", "chunk_similarity",
     "CostCounters", "SparsityMask", "upsample", "topk_row", "mask_from_chunk_scores",
     "prefill_mask", "decode_mask_row", "DecodeSession",
-    "SparseDecoder", "SparsePrefill", "SplitKVShard", "SplitKVGroup",
+    "SparseDecoder", "SparsePrefill", "SplitKVShard", "SplitKVGroup", "predictor",
 ]
 
 

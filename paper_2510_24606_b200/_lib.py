@@ -84,6 +84,9 @@ _SIGS = {
     "dhsa_prefill_attn": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                     C.c_int, C.c_int64, vp, vp, C.c_int, vp, vp, vp, vp]),
     "dhsa_row_quality": (C.c_int, [vp, vp, vp, vp, C.c_int64, C.c_int, vp, vp, vp]),
+    "dhsa_predictor_workspace_size": (C.c_int64, [C.c_int, C.c_int, C.c_int, C.c_int]),
+    "dhsa_predictor_forward": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp,
+                                         vp, vp, vp, C.c_double, vp, vp, vp]),
     "dhsa_attn_stream_workspace_size": (C.c_int64, [C.c_int, C.c_int, C.c_int]),
     "dhsa_attn_stream_counters": (C.c_int, [C.c_int]),
     "dhsa_attn_stream": (C.c_int, [vp, vp, vp, C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int,

@@ -236,6 +236,37 @@ def gen_wire():
     np.save(os.path.join(OUT, "wire_tensor.npy"), t)
 
 
+PREDICTOR_CASES = [  # dim, window, heads, hidden, seed, length, zero_span
+    (32, 4, 8, 256, 0, 100, None),
+    (32, 4, 8, 256, 3, 9, None),        # shortest sequence: one position
+    (16, 3, 4, 24, 5, 61, (10, 30)),    # zero keys: zero encodings, cosine 0
+    (8, 5, 2, 16, 9, 40, None),         # window 5 (25 score lanes), dh 4
+    (64, 2, 2, 32, 1, 70, None),        # dh 32
+]
+
+
+def gen_predictor():
+    from dhsa.predictor import PARAM_ORDER, init_predictor, predict_sequence, save_predictor
+
+    rng = np.random.default_rng(31)
+    blob = {}
+    for c, (dim, w, heads, hidden, seed, L, zero) in enumerate(PREDICTOR_CASES):
+        params = init_predictor(dim, window=w, heads=heads, hidden=hidden, seed=seed)
+        keys = rng.standard_normal((L, dim))
+        if zero:
+            keys[zero[0]:zero[1]] = 0.0
+        pos, p = predict_sequence(keys, params)
+        blob[f"keys_{c}"] = keys
+        blob[f"pos_{c}"] = pos
+        blob[f"p_{c}"] = p
+        blob[f"sha_{c}"] = np.frombuffer(
+            sha(*[params.tensors[n] for n in PARAM_ORDER]).encode(), dtype=np.uint8)
+    blob["cases"] = np.array([c[:6] for c in PREDICTOR_CASES], dtype=np.int64)
+    np.savez_compressed(os.path.join(OUT, "predictor.npz"), **blob)
+    params = init_predictor(8, window=4, heads=2, hidden=16, seed=4)
+    save_predictor(os.path.join(OUT, "predictor_ckpt.prd"), params)
+
+
 def c1_inputs(seed=7):
     """C1 demo shape; regenerated identically by tests (numpy PCG64)."""
     rng = np.random.default_rng(seed)
@@ -293,4 +324,5 @@ if __name__ == "__main__":
     gen_c1()
     gen_nms()
     gen_wire()
+    gen_predictor()
     print("golden fixtures written to", OUT)
