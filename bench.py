@@ -507,34 +507,39 @@ def run_gpu_c5(args):
         tf_peak, tf_sust = d.get("bf16_tflops"), d.get("bf16_tflops_sustained")
     peak = tf_peak or 1590.0
     sweep = []
+
+    def time_prefill(pf):
+        stg = pf.stages(q, k, v, out)
+        for _ in range(W):
+            for _, fn in stg:
+                fn()
+        torch.cuda.synchronize()
+        pf.check_capacity()
+        names = [n for n, _ in stg]
+        acc = {n: 0.0 for n in names}
+        tot = 0.0
+        for _ in range(S):
+            flush.zero_()  # L2 flushed before every timed prefill
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(stg) + 1)]
+            ev[0].record()
+            for i, (_, fn) in enumerate(stg):
+                fn()
+                ev[i + 1].record()
+            torch.cuda.synchronize()
+            for i, n in enumerate(names):
+                acc[n] += ev[i].elapsed_time(ev[i + 1])
+            tot += ev[0].elapsed_time(ev[-1])
+        ms = max_over_ranks(tot / S, world)
+        return ms, {n: acc[n] / S for n in names}
+
     with ClockSampler(local) as clk:
         for K in args.c5_topk:
             pf = SparsePrefill(B, Hq, Hkv, D, L, top_k=K, agg="max")
-            stg = pf.stages(q, k, v, out)
-            for _ in range(W):
-                for _, fn in stg:
-                    fn()
-            torch.cuda.synchronize()
-            pf.check_capacity()
-            names = [n for n, _ in stg]
-            acc = {n: 0.0 for n in names}
-            tot = 0.0
-            for _ in range(S):
-                flush.zero_()  # L2 flushed before every timed prefill
-                ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(stg) + 1)]
-                ev[0].record()
-                for i, (_, fn) in enumerate(stg):
-                    fn()
-                    ev[i + 1].record()
-                torch.cuda.synchronize()
-                for i, n in enumerate(names):
-                    acc[n] += ev[i].elapsed_time(ev[i + 1])
-                tot += ev[0].elapsed_time(ev[-1])
-            ms = max_over_ranks(tot / S, world)
-            attn_ms = acc["attn"] / S
+            ms, bd = time_prefill(pf)
+            attn_ms = bd["attn"]
             fl = pf.flops()
             sweep.append({"top_k": K, "budget": pf.budget, "ms": ms,
-                          "breakdown_ms": {n: acc[n] / S for n in names},
+                          "breakdown_ms": bd,
                           "tflops_algorithmic": fl / 1e12,
                           "attn_tflops": fl / (attn_ms * 1e-3) / 1e12,
                           "attn_frac_of_peak": fl / (attn_ms * 1e-3) / 1e12 / peak,
@@ -563,6 +568,50 @@ def run_gpu_c5(args):
                    "dense_causal_ms": dms, "dense_causal_tflops": dense.flops() / (dms * 1e-3) / 1e12,
                    "note": "harness.attention_mass_recall / output_fidelity semantics over all "
                            "32 heads and 32K rows (the CPU harness needs the 8.6 GB L x L matrix)"}
+    # dynamic chunks (the paper's pipeline): boundary
+    # predictor on the GPU over every kv head's keys -> nms_boundaries on the
+    # host -> per-head chunk lists -> the same prefill with those chunks
+    dynamic = None
+    if not args.no_dynamic:
+        from paper_2510_24606_b200.chunking import nms_boundaries
+        from paper_2510_24606_b200.predictor import BoundaryPredictor, init_predictor
+
+        bp = BoundaryPredictor(init_predictor(D, window=4, heads=8, hidden=256, seed=0))
+        kf = k[0].double().contiguous()
+        for h in range(Hkv):
+            bp.probs(kf[h])
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        probs = [bp.probs(kf[h]) for h in range(Hkv)]
+        e1.record()
+        torch.cuda.synchronize()
+        pred_ms = e0.elapsed_time(e1)
+        t0 = time.perf_counter()
+        bounds = []
+        for p in probs:
+            sc = np.zeros(L)
+            sc[3:L - 4] = p.cpu().numpy()  # predictable positions w-1 .. L-w-1 (w = 4)
+            bounds.append(nms_boundaries(sc, min_conf=0.1, window=32, max_chunks=L // 64))
+        nms_ms = (time.perf_counter() - t0) * 1e3
+        pf = SparsePrefill(B, Hq, Hkv, D, L, top_k=head["top_k"], agg="max", bounds=bounds)
+        ms, bd = time_prefill(pf)
+        fl = pf.flops()
+        lens = np.concatenate([np.diff(b) for b in bounds])
+        dynamic = {"top_k_budget": pf.budget, "ms": ms, "breakdown_ms": bd,
+                   "attn_tflops": fl / (bd["attn"] * 1e-3) / 1e12,
+                   "attn_frac_of_peak": fl / (bd["attn"] * 1e-3) / 1e12 / peak,
+                   "predictor_ms_all_heads": pred_ms, "nms_host_ms_all_heads": nms_ms,
+                   "chunks_per_head": int(np.mean([len(b) - 1 for b in bounds])),
+                   "chunk_len_min_mean_max": [int(lens.min()), float(lens.mean()),
+                                              int(lens.max())],
+                   "note": "random-init predictor (no trained checkpoint offline); fp64 "
+                           "predictor over 8 kv heads x 32K keys; NMS window 32, "
+                           "max_chunks L/64"}
+        if not args.no_quality:
+            rec, cos = mask_quality(q, k, v, pf)
+            dynamic["attention_mass_recall"] = float(rec.mean())
+            dynamic["output_fidelity"] = float(cos.mean())
     result = {
         "metric": "sparse prefill ms per 32K-token sequence (C5); tensor TFLOP/s vs roofline",
         "value": head["ms"], "unit": "ms", "n_gpus": world, "steps": S, "warmup": W,
@@ -576,7 +625,8 @@ def run_gpu_c5(args):
                      "peak": peak, "unit": "TFLOP/s", "frac": head["attn_frac_of_peak"],
                      "peak_source": "measured (MEASURED_PEAKS.json bf16_tflops)" if tf_peak
                      else "fallback (B200_PROFILING.md)", "peak_sustained": tf_sust},
-        "sweep": sweep, "mask_quality": quality, "gpu_launches": 5 * S, "clocks": clk.summary(),
+        "sweep": sweep, "mask_quality": quality, "dynamic_chunks": dynamic,
+        "gpu_launches": 5 * S, "clocks": clk.summary(),
     }
     if rank == 0:
         print(json.dumps(result), flush=True)
@@ -631,6 +681,8 @@ def main():
     ap.add_argument("--cpu-units", type=int, default=None)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-quality", action="store_true")
+    ap.add_argument("--no-dynamic", action="store_true",
+                    help="C5: skip the predictor -> NMS -> dynamic-chunk prefill run")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     # the reference arm: every "step" is one bounded CPU sample (~0.6 s)

@@ -310,27 +310,51 @@ int dhsa_merge_partials(const float* records, int W, int64_t rank_stride, int ro
 int dhsa_prefill_scores(const double* q_centroids, const double* k_centroids, int U, int G,
                         int n_chunks, int D, int agg, double* scores, dhsa_stream_t stream);
 
-/* Plan entries per (selection row, query chunk) needed for `budget`. */
+/* Chunk layout of a prefill.  NULL (or bounds
+ * == NULL) = the static grid [0, block, 2*block, ..., L] (chunking.py:42-54).
+ * Otherwise explicit per-unit boundary lists in check_boundaries form
+ * (chunking.py:23-39; e.g. nms_boundaries over predictor scores,
+ * chunking.py:57-89): unit u = kv head (with batch) has nchunks[u] chunks
+ * bounds[u*bounds_stride + 0..nchunks[u]] (stride 0 = one shared list).  The
+ * attention kernel also needs the query tile table qtiles[u][tiles_per_unit]
+ * = int32 pairs (chunk l, 64-row tile t of chunk l), heaviest first, chunk
+ * -1 = padding; chunk n and tile counts are host-known (prefill.py builds
+ * it). */
+typedef struct {
+  const int32_t* bounds;
+  int64_t bounds_stride;
+  const int32_t* nchunks;
+  const int32_t* qtiles;
+  int32_t tiles_per_unit;
+} dhsa_prefill_chunks;
+
+/* Plan entries per (selection row, query chunk) needed for `budget` on the
+ * static grid (block <= 64). */
 int dhsa_prefill_plan_capacity(int64_t budget, int block);
 
-/* Per (s, query chunk l): the chunks of the walk (masks.topk_row order: score
- * desc, chunk asc) that some row of chunk l takes tokens from, as int32x4
- * {start, len, W, flags} in walk order (W = tokens of non-diagonal chunks
- * ranked before; flags bit0 = the diagonal chunk ranks before, bit1 = this is
- * the diagonal chunk, always last).  Row i of chunk l takes
+/* Per (s, query chunk l): the <= 64-token blocks of the chunks of the walk
+ * (masks.topk_row order: score desc, chunk asc) that some row of chunk l takes
+ * tokens from, as int32x4 {start, len, W, flags}, in walk order (W = tokens of
+ * the whole non-diagonal chunks ranked before, + 64 k for block k of a chunk;
+ * flags bit0 = the diagonal chunk ranks before, bit1 = a block of the diagonal
+ * chunk, those last).  Row i of chunk l (start b_l) takes
  * clamp(R_i - W - (bit0 ? i - b_l : 0), 0, len) lowest tokens of an entry
- * (the diagonal: clamp(R_i - W, 0, i - b_l)) plus self, R_i =
- * min(budget, i+1) - 1 — exactly topk_row on the upsampled row.
- * plans [S][n_chunks][cap] int32x4, nplan [S][n_chunks] (-1 = overflow). */
-int dhsa_prefill_plan(const double* scores, int S, int n_chunks, int L, int block,
-                      int64_t budget, int cap, void* plans, int32_t* nplan,
-                      dhsa_stream_t stream);
+ * (a diagonal block: clamp(min(R_i - W, i - start), 0, len)) plus self, R_i =
+ * min(budget, i+1) - 1 — exactly topk_row on the upsampled row.  s maps to
+ * unit s (agg MAX / MEAN) or s / G (agg NONE) for the chunk layout.
+ * n_chunks = chunk count (static) or the maximum over units (explicit).
+ * plans [S][n_chunks][cap] int32x4, nplan [S][n_chunks] (-1 = overflow,
+ * 0 = chunk l beyond the unit's count). */
+int dhsa_prefill_plan(const double* scores, int S, int G, int agg, int n_chunks, int L,
+                      int block, int64_t budget, const dhsa_prefill_chunks* chunks, int cap,
+                      void* plans, int32_t* nplan, dhsa_stream_t stream);
 
 /* The token sets the plans encode as DHSAMSK1 row bitsets (the reference's
  * mask file payload, serialization.py:80-94): out [S][L][ceil(L/8)] bytes,
  * token t of row i = bit t % 8 of byte t / 8 (self included). */
-int dhsa_prefill_mask_bitsets(const void* plans, const int32_t* nplan, int cap, int S,
-                              int n_chunks, int L, int block, int64_t budget, uint8_t* out,
+int dhsa_prefill_mask_bitsets(const void* plans, const int32_t* nplan, int cap, int S, int G,
+                              int agg, int n_chunks, int L, int block, int64_t budget,
+                              const dhsa_prefill_chunks* chunks, uint8_t* out,
                               dhsa_stream_t stream);
 
 /* Block-sparse attention of every query row over its planned tokens:
@@ -341,9 +365,12 @@ int dhsa_prefill_mask_bitsets(const void* plans, const int32_t* nplan, int cap, 
  * pulling plans, TMEM / barriers / K-V ring kept across plans); NULL -> one
  * CTA per (plan, head slice).  row_stats (float2 [U*G][L], or NULL): per
  * query row the softmax reference max m (log2 domain) and l = sum over the
- * selection of 2^(x - m), x = q.k log2(e) / sqrt(D). */
+ * selection of 2^(x - m), x = q.k log2(e) / sqrt(D).  chunks: as for
+ * dhsa_prefill_plan (explicit bounds: any chunk lengths; query tiles and KV
+ * blocks start at chunk starts, TMA boxes at any row). */
 int dhsa_prefill_attn(const void* q, const void* k, const void* v, int U, int G, int L, int D,
-                      int block, int agg, int64_t budget, const void* plans,
+                      int block, int agg, int64_t budget, int n_chunks,
+                      const dhsa_prefill_chunks* chunks, const void* plans,
                       const int32_t* nplan, int cap, void* out, int32_t* counters,
                       float* row_stats, dhsa_stream_t stream);
 

@@ -33,6 +33,21 @@ class Layout(C.Structure):
     ]
 
 
+class PrefillChunks(C.Structure):
+    """dhsa_prefill_chunks"""
+
+    _fields_ = [
+        ("bounds", vp),
+        ("bounds_stride", C.c_int64),
+        ("nchunks", vp),
+        ("qtiles", vp),
+        ("tiles_per_unit", C.c_int32),
+    ]
+
+
+PChunks = C.POINTER(PrefillChunks)
+
+
 class ShardSpec(C.Structure):
     """dhsa_split_shard"""
     _fields_ = [("chunk_offset", C.c_int32), ("total_chunks", C.c_int32),
@@ -78,11 +93,12 @@ _SIGS = {
                                       vp]),
     "dhsa_prefill_plan_capacity": (C.c_int, [C.c_int64, C.c_int]),
     "dhsa_prefill_mask_bitsets": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
-                                            C.c_int64, vp, vp]),
-    "dhsa_prefill_plan": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int,
-                                    vp, vp, vp]),
+                                            C.c_int, C.c_int, C.c_int64, PChunks, vp, vp]),
+    "dhsa_prefill_plan": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                    C.c_int64, PChunks, C.c_int, vp, vp, vp]),
     "dhsa_prefill_attn": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
-                                    C.c_int, C.c_int64, vp, vp, C.c_int, vp, vp, vp, vp]),
+                                    C.c_int, C.c_int64, C.c_int, PChunks, vp, vp, C.c_int, vp, vp,
+                                    vp, vp]),
     "dhsa_row_quality": (C.c_int, [vp, vp, vp, vp, C.c_int64, C.c_int, vp, vp, vp]),
     "dhsa_predictor_workspace_size": (C.c_int64, [C.c_int, C.c_int, C.c_int, C.c_int]),
     "dhsa_predictor_forward": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp,

@@ -113,28 +113,73 @@ __global__ __launch_bounds__(256) void prefill_scores_kernel(
 
 // ------------------------------------------------------------------- K8 --
 constexpr int kPlanThreads = 128;
+constexpr int kTok = 64;  // KV block / query tile rows of the tcgen05 kernel
 
+// Chunk layout of the prefill: the static grid (bounds == null) or explicit
+// per-unit boundary lists (chunking.check_boundaries form; stride 0 = shared),
+// e.g. nms_boundaries over predictor scores.
+struct PrefillChunks {
+  const int32_t* bounds;   // [U][bstride] or null (static grid)
+  int64_t bstride;
+  const int32_t* nchunks;  // [U] (explicit mode)
+  int block, L;
+  __device__ __forceinline__ int count(int u, int nc) const {
+    return bounds ? nchunks[u] : nc;
+  }
+  __device__ __forceinline__ void range(int u, int l, int& b, int& e) const {
+    if (bounds) {
+      const int32_t* p = bounds + (int64_t)u * bstride;
+      b = p[l];
+      e = p[l + 1];
+    } else {
+      b = l * block;
+      e = min(b + block, L);
+    }
+  }
+};
+
+// Plan entries are <= 64-token KV blocks {start, len, W, flags}: a chunk of
+// which the walk without the diagonal at the largest budget Rmax takes t
+// tokens (an upper bound on every row's take) becomes ceil(t / 64)
+// consecutive blocks (block k: W + 64 k, so a row's take from the chunk is
+// split over its blocks exactly).  The
+// non-diagonal chunks' blocks are written at their walk position (blocks of
+// the chunks ranked before), the diagonal chunk's blocks last; with the static
+// 64 grid every chunk is one block and the entry index is the walk rank.
 __global__ __launch_bounds__(kPlanThreads) void prefill_plan_kernel(
-    const double* __restrict__ S, int nc, int L, int block, int64_t budget, int cap,
-    int4* __restrict__ plans, int32_t* __restrict__ nplan) {
+    const double* __restrict__ S, int nc, PrefillChunks ch, int G, int per_head, int64_t budget,
+    int cap, int4* __restrict__ plans, int32_t* __restrict__ nplan) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ WalkShared sh;
-  __shared__ int s_n;
+  __shared__ int s_n, s_wd, s_nb;
   uint64_t* key = reinterpret_cast<uint64_t*>(smem_raw);
   int32_t* lens = reinterpret_cast<int32_t*>(key + nc);
-  int32_t* list = lens + nc;
+  int32_t* clen = lens + nc;  // full chunk lengths (lens holds the takes)
+  int32_t* list = clen + nc;
   const int l = blockIdx.x, s = blockIdx.y, tid = threadIdx.x;
+  const int u = per_head ? s / G : s;
+  if (l >= ch.count(u, nc)) {
+    if (tid == 0) nplan[(int64_t)s * nc + l] = 0;
+    return;
+  }
   const double* srow = S + ((int64_t)s * nc + l) * nc;
-  const int bl = l * block, el = min(bl + block, L);
+  int bl, el;
+  ch.range(u, l, bl, el);
   // the largest token budget among the rows of chunk l (its last row)
   const int64_t rmax64 = (budget < (int64_t)el ? budget : (int64_t)el) - 1;
   const uint32_t Rmax = (uint32_t)rmax64;
   for (int c = tid; c < l; c += kPlanThreads) {
     key[c] = order_key(srow[c]);
-    lens[c] = block;  // chunks before the diagonal are full
+    int b, e;
+    ch.range(u, c, b, e);
+    lens[c] = clen[c] = e - b;  // chunks before the diagonal are whole
   }
   const uint64_t kdiag = order_key(srow[l]);
-  if (tid == 0) s_n = 0;
+  if (tid == 0) {
+    s_n = 0;
+    s_wd = 0;
+    s_nb = 0;
+  }
   __syncthreads();
   // takes of the walk over the non-diagonal chunks with budget Rmax
   if (l > 0) {
@@ -155,36 +200,60 @@ __global__ __launch_bounds__(kPlanThreads) void prefill_plan_kernel(
   __syncthreads();
   const int n = s_n;
   int4* out = plans + ((int64_t)s * nc + l) * cap;
-  // rank = position in the walk order; W = full chunk tokens ranked before
-  int wdiag_local = 0;
+  // walk position: W = whole-chunk tokens ranked before, pos = their blocks
+  int wd = 0, nb = 0;
   for (int i = tid; i < n; i += kPlanThreads) {
     const int c = list[i];
     const uint64_t kc = key[c];
-    int rank = 0;
+    int W = 0, pos = 0;
     for (int j = 0; j < n; ++j) {
       const int cj = list[j];
       const uint64_t kj = key[cj];
-      rank += (kj > kc || (kj == kc && cj < c)) ? 1 : 0;
+      if (kj > kc || (kj == kc && cj < c)) {
+        W += clen[cj];
+        pos += (lens[cj] + kTok - 1) / kTok;
+      }
     }
-    // every selected chunk is full (block tokens); W = rank * block
+    int b, e;
+    ch.range(u, c, b, e);
     const int diag_before = kdiag > kc ? 1 : 0;  // tie: the lower index (c < l) first
-    if (rank < cap - 1) out[rank] = make_int4(c * block, block, rank * block, diag_before);
-    if (!diag_before) wdiag_local += block;
+    // only the blocks some row can reach
+    const int nbk = (lens[c] + kTok - 1) / kTok;
+    for (int k = 0; k < nbk; ++k)
+      if (pos + k < cap) out[pos + k] = make_int4(b + k * kTok, min(kTok, clen[c] - k * kTok),
+                                                  W + k * kTok, diag_before);
+    if (!diag_before) wd += clen[c];
+    nb += nbk;
   }
-  wdiag_local = warp_sum(wdiag_local);
-  __shared__ int s_wd;
-  if (tid == 0) s_wd = 0;
-  __syncthreads();
-  if ((tid & 31) == 0 && wdiag_local) atomicAdd(&s_wd, wdiag_local);
-  __syncthreads();
-  if (tid == 0) {
-    if (n + 1 > cap) {
-      nplan[s * nc + l] = -1;  // capacity error (reported by the host)
-    } else {
-      out[n] = make_int4(bl, el - bl, s_wd, 2);  // the diagonal chunk (self always)
-      nplan[s * nc + l] = n + 1;
-    }
+  wd = warp_sum(wd);
+  nb = warp_sum(nb);
+  if ((tid & 31) == 0) {
+    if (wd) atomicAdd(&s_wd, wd);
+    if (nb) atomicAdd(&s_nb, nb);
   }
+  __syncthreads();
+  const int nbt = s_nb, nd = (el - bl + kTok - 1) / kTok;
+  if (nbt + nd > cap) {
+    if (tid == 0) nplan[(int64_t)s * nc + l] = -1;  // capacity error (reported by the host)
+    return;
+  }
+  for (int k = tid; k < nd; k += kPlanThreads)  // the diagonal chunk (self always)
+    out[nbt + k] = make_int4(bl + k * kTok, min(kTok, el - bl - k * kTok), s_wd + k * kTok, 2);
+  if (tid == 0) nplan[(int64_t)s * nc + l] = nbt + nd;
+}
+
+// Tokens row i takes from plan entry e: the lowest
+// clamp(R_i - W - [diag before] d_i, 0, len) of a non-diagonal block, where
+// d_i = i - (chunk start) is the diagonal chunk's effective length; of a
+// diagonal block the lowest clamp(R_i - W, 0, i - start) (causal), plus self.
+__device__ __forceinline__ int entry_take(int4 e, int Ri, int i, int dl, int& self) {
+  if (e.w & 2) {
+    const int db = i - e.x;
+    self = (db >= 0 && db < e.y) ? db : -1;
+    return max(0, min(min(Ri - e.z, db), e.y));
+  }
+  self = -1;
+  return max(0, min(Ri - e.z - ((e.w & 1) ? dl : 0), e.y));
 }
 
 // ------------------------------------------------------------------- K9 --
@@ -202,6 +271,21 @@ struct PrefillArgs {
   int32_t* counters;   // [2] plan pull counter, exits (persistent kernel); zero at rest
   float2* row_stats;   // [q heads][L] (m, l): the row's softmax reference max (log2
                        // domain) and sum of 2^(x - m) over its selection, or null
+  PrefillChunks ch;    // chunk layout (static grid or explicit bounds)
+  const int2* qtiles;  // explicit bounds: [U][T] query tiles (chunk l, 64-row tile t),
+  int T;               // heavy first, l = -1 pads; null with the static grid (T = nc)
+  // query tile y of unit u -> (chunk l, tile t); false for padding
+  __device__ __forceinline__ bool tile(int u, int y, int& l, int& t) const {
+    if (qtiles) {
+      const int2 q = qtiles[(int64_t)u * T + y];
+      l = q.x;
+      t = q.y;
+      return l >= 0;
+    }
+    l = nc - 1 - y;  // heavy (late) query chunks first
+    t = 0;
+    return true;
+  }
 };
 
 template <int MT, int NST>
@@ -258,15 +342,20 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_kernel(
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int hs = blockIdx.x;                   // head slice of the selection row
-  const int l = a.nc - 1 - blockIdx.y;         // heavy (late) query chunks first
   const int s = blockIdx.z;                    // selection row
   const int unit = a.per_head ? s / a.G : s;   // kv head (with batch)
   const int qh0 = (a.per_head ? s : s * a.G) + hs * a.heads_per_cta;  // first q head
   const int nh = a.per_head ? 1 : min(a.heads_per_cta, a.G - hs * a.heads_per_cta);
-  const int bl = l * a.block;
-  const int np = __ldg(a.nplan + (int64_t)s * a.nc + l);
+  int l, qt;
+  if (!a.tile(unit, blockIdx.y, l, qt)) return;
+  int bl, el;
+  a.ch.range(unit, l, bl, el);
+  const int row0 = bl + qt * kTok;             // first query row of the tile
+  const int npl = __ldg(a.nplan + (int64_t)s * a.nc + l);
   const int4* plan = a.plans + ((int64_t)s * a.nc + l) * a.cap;
-  if (np <= 0) return;  // capacity overflow (nplan = -1): reported by the host
+  if (npl <= 0) return;  // capacity overflow (nplan = -1): reported by the host
+  // diagonal blocks after the tile's own are causal-masked for all its rows
+  const int np = npl - (el - bl + kTok - 1) / kTok + qt + 1;
   for (int e = threadIdx.x; e < np && e < kPlanCap; e += blockDim.x) s_plan[e] = plan[e];
 
   if (threadIdx.x == 0) {
@@ -299,7 +388,7 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_kernel(
       mbar_expect_tx(&q_full, SM::Q);
       for (int rg = 0; rg < 2 * MT; ++rg) {
         const int h = qh0 + (rg < nh ? rg : 0);  // padding row groups repeat a live head
-        const int row = h * a.L + bl;
+        const int row = h * a.L + row0;
         for (int half = 0; half < 2; ++half)
           tma_load_2d(smem + SM::q_off + (rg >> 1) * 32768 + half * 16384 + (rg & 1) * 8192, &tmQ,
                       &q_full, half * 64, row);
@@ -368,8 +457,8 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_kernel(
     const int trow = quad * 32 + lane;      // row within the M tile (= TMEM lane)
     const int r = mt * 128 + trow;          // row within the CTA tile
     const int rg = r >> 6;                  // row group = head slot
-    const int i = bl + (r & 63);            // token index of this query row
-    const bool live = rg < nh && i < a.L;
+    const int i = row0 + (r & 63);          // token index of this query row
+    const bool live = rg < nh && i < el;
     const int64_t keep = a.budget < (int64_t)i + 1 ? a.budget : (int64_t)i + 1;
     const int Ri = (int)(keep - 1);
     const int dl = i - bl;
@@ -379,14 +468,8 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_kernel(
     const float sl2 = a.scale_log2;
     float m_used = -INFINITY, lsum = 0.f;
     for (int j = 0; j < np; ++j) {
-      const int4 e = s_plan[j];
-      int lim, self = -1;
-      if (e.w & 2) {
-        lim = max(0, min(Ri - e.z, dl));
-        self = dl;
-      } else {
-        lim = max(0, min(Ri - e.z - ((e.w & 1) ? dl : 0), e.y));
-      }
+      int self;
+      int lim = entry_take(s_plan[j], Ri, i, dl, self);
       if (!live) {
         lim = 0;
         self = -1;
@@ -506,9 +589,10 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_persist_kernel(
   __shared__ uint32_t s_tmem;
   __shared__ int4 s_plan[2][kPlanCap];
   __shared__ int4 s_meta[2];  // (plan id or -1, entries, l, s * slices + hs)
+  __shared__ int s_qt[2];     // query tile within the chunk
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int total = a.S * a.nc * a.slices;
+  const int total = a.S * (a.qtiles ? a.T : a.nc) * a.slices;
   if (threadIdx.x == 0) {
     for (int i = 0; i < NST; ++i) {
       mbar_init(&kv_full[i], 1);
@@ -533,11 +617,11 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_persist_kernel(
   const uint32_t tmem = s_tmem;
   const uint32_t sq = smem_u32(smem + SM::q_off);
   const uint32_t skv = smem_u32(smem + SM::kv_off);
-  // plan p -> (query chunk l, selection row s, head slice hs), heavy first
-  auto decode = [&](int p, int& l, int& sr, int& hs) {
+  // plan p -> (query tile y, selection row s, head slice hs), heavy first
+  auto decode = [&](int p, int& y, int& sr, int& hs) {
     const int per_l = a.S * a.slices;
-    l = a.nc - 1 - p / per_l;
-    const int r = p - (a.nc - 1 - l) * per_l;
+    y = p / per_l;
+    const int r = p - y * per_l;
     sr = r / a.slices;
     hs = r - sr * a.slices;
   };
@@ -564,25 +648,33 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_persist_kernel(
         }
         break;
       }
-      int l, sr, hs;
-      decode(p, l, sr, hs);
-      const int np = __ldg(a.nplan + (int64_t)sr * a.nc + l);
+      int y, sr, hs, l = 0, qt = 0;
+      decode(p, y, sr, hs);
+      const int unit = a.per_head ? sr / a.G : sr;
+      int np = 0, bl = 0, el = 0;
+      if (a.tile(unit, y, l, qt)) {
+        a.ch.range(unit, l, bl, el);
+        np = __ldg(a.nplan + (int64_t)sr * a.nc + l);
+        if (np > 0) np = np - (el - bl + kTok - 1) / kTok + qt + 1;
+      }
       const int4* plan = a.plans + ((int64_t)sr * a.nc + l) * a.cap;
       for (int e = lane; e < np && e < kPlanCap; e += 32) s_plan[b][e] = __ldg(plan + e);
-      if (lane == 0) s_meta[b] = make_int4(p, np, l, sr * a.slices + hs);
+      if (lane == 0) {
+        s_meta[b] = make_int4(p, np, l, sr * a.slices + hs);
+        s_qt[b] = qt;
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&plan_full[b]);
       if (np <= 0) continue;  // capacity overflow: reported by the host
       if (lane == 0) {
-        const int unit = a.per_head ? sr / a.G : sr;
         const int qh0 = (a.per_head ? sr : sr * a.G) + hs * a.heads_per_cta;
         const int nh = a.per_head ? 1 : min(a.heads_per_cta, a.G - hs * a.heads_per_cta);
-        const int bl = l * a.block;
+        const int row0 = bl + qt * kTok;
         if (kq >= 1) mbar_wait(&q_empty, (kq - 1) & 1);  // every S of the previous plan done
         mbar_expect_tx(&q_full, SM::Q);
         for (int rg = 0; rg < 2 * MT; ++rg) {
           const int h = qh0 + (rg < nh ? rg : 0);
-          const int row = h * a.L + bl;
+          const int row = h * a.L + row0;
           for (int half = 0; half < 2; ++half)
             tma_load_2d(smem + SM::q_off + (rg >> 1) * 32768 + half * 16384 + (rg & 1) * 8192, &tmQ,
                         &q_full, half * 64, row);
@@ -693,23 +785,18 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_persist_kernel(
       const int l = m.z, sr = m.w / a.slices, hs = m.w - sr * a.slices;
       const int qh0 = (a.per_head ? sr : sr * a.G) + hs * a.heads_per_cta;
       const int nh = a.per_head ? 1 : min(a.heads_per_cta, a.G - hs * a.heads_per_cta);
-      const int bl = l * a.block;
-      const int i = bl + (r & 63);
-      const bool live = rg < nh && i < a.L;
+      int bl, el;
+      a.ch.range(a.per_head ? sr / a.G : sr, l, bl, el);
+      const int i = bl + s_qt[b] * kTok + (r & 63);
+      const bool live = rg < nh && i < el;
       const int64_t keep = a.budget < (int64_t)i + 1 ? a.budget : (int64_t)i + 1;
       const int Ri = (int)(keep - 1);
       const int dl = i - bl;
       float m_used = -INFINITY, lsum = 0.f;
       for (int j = 0; j < np; ++j) {
         const int jj = jg0 + j;
-        const int4 e = s_plan[b][j];
-        int lim, self = -1;
-        if (e.w & 2) {
-          lim = max(0, min(Ri - e.z, dl));
-          self = dl;
-        } else {
-          lim = max(0, min(Ri - e.z - ((e.w & 1) ? dl : 0), e.y));
-        }
+        int self;
+        int lim = entry_take(s_plan[b][j], Ri, i, dl, self);
         if (!live) {
           lim = 0;
           self = -1;
@@ -827,7 +914,7 @@ static int launch_prefill_persist(const CUtensorMap& mq, const CUtensorMap& mk,
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int total = a.S * a.nc * a.slices;
+  const int total = a.S * (a.qtiles ? a.T : a.nc) * a.slices;
   const int grid = total < sms ? total : sms;
   kern<<<grid, 64 + 128 * MT, SM::total, st>>>(mq, mk, mv, a);
   return check_launch("dhsa_prefill_attn");
@@ -843,7 +930,7 @@ static int launch_prefill_attn(const CUtensorMap& mq, const CUtensorMap& mk, con
     set_error("dhsa_prefill_attn: %s", cudaGetErrorString(e));
     return DHSA_ECUDA;
   }
-  dim3 grid((unsigned)a.slices, (unsigned)a.nc, (unsigned)S);
+  dim3 grid((unsigned)a.slices, (unsigned)(a.qtiles ? a.T : a.nc), (unsigned)S);
   kern<<<grid, 64 + 128 * MT, SM::total, st>>>(mq, mk, mv, a);
   return check_launch("dhsa_prefill_attn");
 }
@@ -855,15 +942,20 @@ static int launch_prefill_attn(const CUtensorMap& mq, const CUtensorMap& mk, con
 // is assembled in shared memory with word atomics and streamed out.
 __global__ __launch_bounds__(128) void plan_bitsets_kernel(const int4* __restrict__ plans,
                                                            const int32_t* __restrict__ nplan,
-                                                           int cap, int nc, int L, int block,
-                                                           int64_t budget, int64_t nbytes,
+                                                           int cap, int nc, PrefillChunks ch,
+                                                           int G, int per_head, int64_t budget,
+                                                           int64_t nbytes,
                                                            uint8_t* __restrict__ out) {
   extern __shared__ uint32_t rowbits[];
   const int l = blockIdx.x, s = blockIdx.y, tid = threadIdx.x;
+  const int u = per_head ? s / G : s;
+  if (l >= ch.count(u, nc)) return;
+  const int L = ch.L;
   const int np = nplan[(int64_t)s * nc + l];
   const int4* plan = plans + ((int64_t)s * nc + l) * cap;
   const int nwords = (int)((nbytes + 3) / 4);
-  const int bl = l * block, el = min(bl + block, L);
+  int bl, el;
+  ch.range(u, l, bl, el);
   for (int i = bl; i < el; ++i) {
     for (int w = tid; w < nwords; w += 128) rowbits[w] = 0u;
     __syncthreads();
@@ -871,8 +963,8 @@ __global__ __launch_bounds__(128) void plan_bitsets_kernel(const int4* __restric
     const int Ri = (int)(keep - 1), dl = i - bl;
     for (int e = tid; e < np; e += 128) {
       const int4 en = plan[e];
-      const int lim = (en.w & 2) ? max(0, min(Ri - en.z, dl))
-                                 : max(0, min(Ri - en.z - ((en.w & 1) ? dl : 0), en.y));
+      int self;
+      const int lim = entry_take(en, Ri, i, dl, self);
       for (int t = en.x; t < en.x + lim;) {  // word-sized pieces of [start, start + lim)
         const int w = t >> 5, b0 = t & 31;
         const int n = min(32 - b0, en.x + lim - t);
@@ -938,12 +1030,43 @@ extern "C" int dhsa_row_quality(const float* stats_sel, const float* stats_all,
   return check_launch("dhsa_row_quality");
 }
 
+// Chunk layout from the C struct (null = static grid of `block`).
+static PrefillChunks make_chunks(const dhsa_prefill_chunks* c, int block, int L) {
+  PrefillChunks ch{};
+  ch.block = block;
+  ch.L = L;
+  if (c && c->bounds) {
+    ch.bounds = c->bounds;
+    ch.bstride = c->bounds_stride;
+    ch.nchunks = c->nchunks;
+  }
+  return ch;
+}
+
+static int check_chunks(const dhsa_prefill_chunks* c, int n_chunks, int L, int block,
+                        bool need_tiles, const char* who) {
+  if (c && c->bounds) {
+    DHSA_REQUIRE(c->nchunks, "%s: explicit bounds need nchunks", who);
+    DHSA_REQUIRE(c->bounds_stride == 0 || c->bounds_stride >= n_chunks + 1,
+                 "%s: bounds_stride must be 0 or >= n_chunks + 1", who);
+    DHSA_REQUIRE(!need_tiles || (c->qtiles && c->tiles_per_unit >= 1),
+                 "%s: explicit bounds need the query tile table", who);
+  } else {
+    DHSA_REQUIRE((int64_t)(n_chunks - 1) * block < L && (int64_t)n_chunks * block >= L,
+                 "%s: n_chunks does not match L / block", who);
+  }
+  return DHSA_OK;
+}
+
 extern "C" int dhsa_prefill_mask_bitsets(const void* plans, const int32_t* nplan, int cap, int S,
-                                         int n_chunks, int L, int block, int64_t budget,
+                                         int G, int agg, int n_chunks, int L, int block,
+                                         int64_t budget, const dhsa_prefill_chunks* chunks,
                                          uint8_t* out, dhsa_stream_t stream) {
-  DHSA_REQUIRE(plans && nplan && out && S >= 1 && n_chunks >= 1 && L >= 1 && block >= 1,
+  DHSA_REQUIRE(plans && nplan && out && S >= 1 && G >= 1 && n_chunks >= 1 && L >= 1 && block >= 1,
                "dhsa_prefill_mask_bitsets: bad arguments");
   DHSA_REQUIRE(budget >= 1, "budget must be >= 1");
+  int rc = check_chunks(chunks, n_chunks, L, block, false, "dhsa_prefill_mask_bitsets");
+  if (rc) return rc;
   const int64_t nbytes = ((int64_t)L + 7) / 8;
   const size_t smem = (size_t)((nbytes + 3) / 4) * 4;
   DHSA_REQUIRE(smem <= 200 * 1024, "dhsa_prefill_mask_bitsets: L too large (%d)", L);
@@ -957,7 +1080,8 @@ extern "C" int dhsa_prefill_mask_bitsets(const void* plans, const int32_t* nplan
   }
   dim3 grid((unsigned)n_chunks, (unsigned)S);
   plan_bitsets_kernel<<<grid, 128, smem, (cudaStream_t)stream>>>(
-      (const int4*)plans, nplan, cap, n_chunks, L, block, budget, nbytes, out);
+      (const int4*)plans, nplan, cap, n_chunks, make_chunks(chunks, block, L), G,
+      agg == DHSA_AGG_NONE, budget, nbytes, out);
   return check_launch("dhsa_prefill_mask_bitsets");
 }
 
@@ -979,20 +1103,21 @@ extern "C" int dhsa_prefill_scores(const double* q_centroids, const double* k_ce
 }
 
 extern "C" int dhsa_prefill_plan_capacity(int64_t budget, int block) {
-  if (budget < 1 || block < 1) return -1;
+  if (budget < 1 || block < 1 || block > kTok) return -1;
   return (int)((budget - 1 + block - 1) / block) + 2;
 }
 
-extern "C" int dhsa_prefill_plan(const double* scores, int S, int n_chunks, int L, int block,
-                                 int64_t budget, int cap, void* plans, int32_t* nplan,
-                                 dhsa_stream_t stream) {
-  DHSA_REQUIRE(scores && plans && nplan && S >= 1 && n_chunks >= 1 && block >= 1 && L >= 1,
+extern "C" int dhsa_prefill_plan(const double* scores, int S, int G, int agg, int n_chunks, int L,
+                                 int block, int64_t budget, const dhsa_prefill_chunks* chunks,
+                                 int cap, void* plans, int32_t* nplan, dhsa_stream_t stream) {
+  DHSA_REQUIRE(scores && plans && nplan && S >= 1 && G >= 1 && n_chunks >= 1 && block >= 1 &&
+                   L >= 1,
                "dhsa_prefill_plan: bad arguments");
   DHSA_REQUIRE(budget >= 1, "budget must be >= 1");
-  DHSA_REQUIRE((int64_t)(n_chunks - 1) * block < L && (int64_t)n_chunks * block >= L,
-               "dhsa_prefill_plan: n_chunks does not match L / block");
+  int rc = check_chunks(chunks, n_chunks, L, block, false, "dhsa_prefill_plan");
+  if (rc) return rc;
   DHSA_REQUIRE(cap >= 2, "dhsa_prefill_plan: capacity too small");
-  const size_t smem = (size_t)n_chunks * (8 + 4 + 4);
+  const size_t smem = (size_t)n_chunks * (8 + 4 + 4 + 4);
   DHSA_REQUIRE(smem <= 200 * 1024, "dhsa_prefill_plan: too many chunks (%d)", n_chunks);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(prefill_plan_kernel,
@@ -1004,17 +1129,23 @@ extern "C" int dhsa_prefill_plan(const double* scores, int S, int n_chunks, int 
   }
   dim3 grid((unsigned)n_chunks, (unsigned)S);
   prefill_plan_kernel<<<grid, kPlanThreads, smem, (cudaStream_t)stream>>>(
-      scores, n_chunks, L, block, budget, cap, (int4*)plans, nplan);
+      scores, n_chunks, make_chunks(chunks, block, L), G, agg == DHSA_AGG_NONE, budget, cap,
+      (int4*)plans, nplan);
   return check_launch("dhsa_prefill_plan");
 }
 
 extern "C" int dhsa_prefill_attn(const void* q, const void* k, const void* v, int U, int G, int L,
-                                 int D, int block, int agg, int64_t budget, const void* plans,
+                                 int D, int block, int agg, int64_t budget, int n_chunks,
+                                 const dhsa_prefill_chunks* chunks, const void* plans,
                                  const int32_t* nplan, int cap, void* out, int32_t* counters,
                                  float* row_stats, dhsa_stream_t stream) {
   DHSA_REQUIRE(q && k && v && plans && nplan && out, "dhsa_prefill_attn: null pointer");
   DHSA_REQUIRE(D == 128, "dhsa_prefill_attn: head_dim must be 128 (got %d)", D);
-  DHSA_REQUIRE(block == 64, "dhsa_prefill_attn: the tcgen05 tiles need 64-token chunks");
+  const bool explicit_bounds = chunks && chunks->bounds;
+  DHSA_REQUIRE(explicit_bounds || block == 64,
+               "dhsa_prefill_attn: the static grid needs 64-token chunks");
+  int rc0 = check_chunks(chunks, n_chunks, L, block, true, "dhsa_prefill_attn");
+  if (rc0) return rc0;
   DHSA_REQUIRE(U >= 1 && G >= 1 && L >= 1 && cap >= 2 && cap <= kPlanCap,
                "dhsa_prefill_attn: bad shape (plan capacity <= %d)", kPlanCap);
   DHSA_REQUIRE(budget >= 1, "budget must be >= 1");
@@ -1034,8 +1165,13 @@ extern "C" int dhsa_prefill_attn(const void* q, const void* k, const void* v, in
   a.plans = (const int4*)plans;
   a.nplan = nplan;
   a.cap = cap;
-  a.nc = (L + block - 1) / block;
+  a.nc = n_chunks;
   a.L = L;
+  a.ch = make_chunks(chunks, block, L);
+  if (explicit_bounds) {
+    a.qtiles = reinterpret_cast<const int2*>(chunks->qtiles);
+    a.T = chunks->tiles_per_unit;
+  }
   a.block = block;
   a.budget = budget;
   a.G = G;

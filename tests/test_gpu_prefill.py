@@ -36,29 +36,36 @@ def _inputs(B, Hq, Hkv, L, D, seed, kind="normal"):
 
 
 def _run(B, Hq, Hkv, L, top_k=None, budget=None, agg="max", seed=0, kind="normal",
-         check_rows=None, check_out=True):
+         check_rows=None, check_out=True, bounds=None):
+    """``bounds``: None (static grid), one list, or one list per kv unit."""
     from paper_2510_24606_b200.prefill import SparsePrefill
 
     D = 128
     G = Hq // Hkv
     t, host = _inputs(B, Hq, Hkv, L, D, seed, kind)
-    pf = SparsePrefill(B, Hq, Hkv, D, L, top_k=top_k or 4, budget=budget, agg=agg)
+    pf = SparsePrefill(B, Hq, Hkv, D, L, top_k=top_k or 4, budget=budget, agg=agg,
+                       bounds=bounds)
     out = pf(t["q"].cuda(), t["k"].cuda(), t["v"].cuda())
     torch.cuda.synchronize()
     pf.check_capacity()
     o = out.double().cpu().numpy()
-    bounds = O.static_grid(L, 64)
     hp = pf.host_plans()
     worst = 0.0
     for b in range(B):
         for h in range(Hkv):
             u = b * Hkv + h
+            if bounds is None:
+                ub = O.static_grid(L, 64)
+            elif np.isscalar(bounds[0]):
+                ub = list(bounds)
+            else:
+                ub = list(bounds[u])
             qh = host["q"][b, h * G:(h + 1) * G]
             kh = np.repeat(host["k"][b, h][None], G, axis=0)
             if agg == "none":
-                per = [O.prefill_rows(qh[j], kh[j], bounds, pf.budget) for j in range(G)]
+                per = [O.prefill_rows(qh[j], kh[j], ub, pf.budget) for j in range(G)]
             else:
-                rows = O.prefill_rows(qh, kh, bounds, pf.budget, agg=agg)
+                rows = O.prefill_rows(qh, kh, ub, pf.budget, agg=agg)
                 per = [rows] * G
             check = range(L) if check_rows is None else check_rows
             for j in range(G):
@@ -182,3 +189,102 @@ def test_mask_quality_matches_reference_metrics(agg):
         assert abs(rec[0, h].mean() - r_ref.mean()) <= 2e-3
         assert np.abs(cos[0, h] - c_ref).max() <= 1e-2
         assert abs(cos[0, h].mean() - c_ref.mean()) <= 2e-3
+
+
+# ------------------------------------------- dynamic chunks (8f row 1) --
+
+def _rand_bounds(rng, L, short=True, long=True):
+    """Random boundary list mixing 1..63-token, 64-aligned and > 64-token
+    chunks (up to 300 tokens)."""
+    b, pos = [0], 0
+    while pos < L:
+        r = rng.random()
+        if short and r < 0.35:
+            n = int(rng.integers(1, 64))
+        elif long and r < 0.7:
+            n = int(rng.integers(65, 300))
+        else:
+            n = 64 * int(rng.integers(1, 3))
+        pos = min(L, pos + n)
+        b.append(pos)
+    return b
+
+
+@pytest.mark.parametrize("budget", [1, 50, 257, 700, 3000])
+def test_prefill_dynamic_shared_bounds(budget):
+    """One explicit boundary list (short, long and aligned chunks) for every
+    unit: rows index-exact, outputs within tolerance."""
+    rng = np.random.default_rng(budget)
+    L = 1500
+    worst = _run(B=1, Hq=4, Hkv=1, L=L, budget=budget, agg="max", seed=budget,
+                 bounds=_rand_bounds(rng, L), check_rows=range(L))
+    assert worst <= TOL_BF16, worst
+
+
+@pytest.mark.parametrize("agg", ["max", "mean", "none"])
+def test_prefill_dynamic_per_unit_bounds(agg):
+    """A different boundary list per kv unit (B=2 x Hkv=2)."""
+    rng = np.random.default_rng(5)
+    L = 1200
+    bounds = [_rand_bounds(rng, L) for _ in range(4)]
+    worst = _run(B=2, Hq=8, Hkv=2, L=L, budget=400, agg=agg, seed=13, bounds=bounds,
+                 check_rows=range(0, L, 3))
+    assert worst <= TOL_BF16, worst
+
+
+def test_prefill_dynamic_nms_bounds():
+    """Boundaries from nms_boundaries over per-position scores (the paper's
+    pipeline: predictor scores -> NMS -> chunks)."""
+    from paper_2510_24606_b200.chunking import nms_boundaries
+
+    rng = np.random.default_rng(8)
+    L = 2048
+    bounds = nms_boundaries(rng.random(L), min_conf=0.2, window=24, max_chunks=40)
+    worst = _run(B=1, Hq=4, Hkv=1, L=L, budget=513, agg="max", seed=8, bounds=bounds,
+                 check_rows=range(0, L, 2))
+    assert worst <= TOL_BF16, worst
+
+
+@pytest.mark.parametrize("case", ["one_chunk", "singletons", "ties"])
+def test_prefill_dynamic_extremes(case):
+    """One chunk of the whole sequence (diagonal blocks only, many query
+    tiles), all-singleton chunks (one token each), and exact score ties over
+    unequal chunks."""
+    rng = np.random.default_rng(3)
+    if case == "one_chunk":
+        L, bounds, budget, kind = 1000, [0, 1000], 300, "normal"
+    elif case == "singletons":
+        L, bounds, budget, kind = 300, list(range(301)), 65, "normal"
+    else:
+        L, budget, kind = 768, 200, "ties"
+        bounds = [0, 64, 128, 192, 250, 400, 401, 530, 768]
+    worst = _run(B=1, Hq=4, Hkv=1, L=L, budget=budget, agg="max", seed=4, kind=kind,
+                 bounds=bounds, check_rows=range(L))
+    assert worst <= TOL_BF16, worst
+
+
+@pytest.mark.parametrize("persistent", ["0", "1"])
+def test_prefill_dynamic_both_grids(persistent, monkeypatch):
+    monkeypatch.setenv("DHSA_PREFILL_PERSISTENT", persistent)
+    rng = np.random.default_rng(21)
+    L = 2000
+    bounds = [_rand_bounds(rng, L) for _ in range(2)]
+    worst = _run(B=1, Hq=8, Hkv=2, L=L, budget=600, agg="max", seed=21, bounds=bounds,
+                 check_rows=range(0, L, 7))
+    assert worst <= TOL_BF16, worst
+
+
+def test_prefill_dynamic_mask_export():
+    """Device bitsets of a dynamic-chunk plan equal the oracle rows."""
+    from paper_2510_24606_b200 import serialization as S
+    from paper_2510_24606_b200.prefill import SparsePrefill
+
+    rng = np.random.default_rng(2)
+    L = 700
+    bounds = _rand_bounds(rng, L)
+    t, host = _inputs(1, 4, 1, L, 128, 2)
+    pf = SparsePrefill(1, 4, 1, 128, L, budget=150, agg="max", bounds=bounds)
+    pf(t["q"].cuda(), t["k"].cuda(), t["v"].cuda())
+    bits = pf.mask_bitsets().cpu().numpy()[0]
+    rows = O.prefill_rows(host["q"][0], np.repeat(host["k"][0], 4, axis=0), bounds, 150)
+    assert np.array_equal(bits, S.rows_to_bitsets(L, rows))
