@@ -51,10 +51,37 @@ def shard_ranges(prompt_len: int, block: int, world: int):
     return out
 
 
-def candidate_capacity(budget: int, block: int) -> int:
+def shard_chunks(bounds, world: int):
+    """Contiguous chunk ranges [(c0, c1)] of the W shards for an explicit
+    boundary list: cuts at the chunk starts
+    nearest to an even token split, at least one chunk per shard."""
+    b = [int(x) for x in bounds]
+    nc = len(b) - 1
+    if nc < world:
+        raise ValueError(f"{nc} chunks cannot be split over {world} shards")
+    cuts = [0]
+    for r in range(1, world):
+        target = b[-1] * r / world
+        c = min(range(nc + 1), key=lambda j: (abs(b[j] - target), j))
+        c = max(c, cuts[-1] + 1)
+        c = min(c, nc - (world - r))
+        cuts.append(c)
+    cuts.append(nc)
+    return [(cuts[r], cuts[r + 1]) for r in range(world)]
+
+
+def candidate_capacity(budget: int, block: int, lengths=None) -> int:
     """Upper bound on chunks with a positive take in a walk of budget-1
-    tokens over static ``block`` chunks + the generated chunk."""
-    return (budget - 1) // block + 4
+    tokens + the generated chunk: static ``block`` chunks, or the local chunk
+    ``lengths`` (the walk touches at most one chunk more than the shortest
+    chunks whose lengths stay below budget-1)."""
+    if lengths is None:
+        return (budget - 1) // block + 4
+    import numpy as np
+
+    srt = np.cumsum(np.sort(np.asarray(lengths, dtype=np.int64)))
+    m = int(np.searchsorted(srt, budget - 1, side="left"))
+    return min(m + 1, len(srt)) + 3
 
 
 class TorchComm:
@@ -91,16 +118,32 @@ class SplitKVShard:
     """One shard of a sequence-sharded sparse decode (bf16 sketch path).
 
     ``prompt_len`` is the GLOBAL prompt length; the shard's range comes from
-    ``shard_ranges``.  Every shard receives the full q [B, Hq, D] each step;
+    ``shard_ranges`` (static grid) or ``shard_chunks`` (``bounds``: one
+    explicit boundary list shared by every unit; the shard gets its chunks,
+    re-based to its first token, and global chunk ids keep the reference's
+    tie-break).  Every shard receives the full q [B, Hq, D] each step;
     only the tail shard receives k_new / v_new."""
 
     def __init__(self, batch, q_heads, kv_heads, head_dim, prompt_len, *, rank, world,
                  block=64, top_k=64, budget=None, agg="max", max_new=1024, tile=64,
-                 splits=None, device=None, attn_mode=None):
+                 splits=None, device=None, attn_mode=None, bounds=None):
         self.rank, self.world = int(rank), int(world)
         self.block = int(block)
         self.total_prompt = int(prompt_len)
-        self.lo, self.hi = shard_ranges(self.total_prompt, self.block, self.world)[self.rank]
+        self.local_bounds = None
+        max_chunks = None
+        if bounds is None:
+            self.lo, self.hi = shard_ranges(self.total_prompt, self.block, self.world)[self.rank]
+            c0, n_total = self.lo // self.block, (self.total_prompt + self.block - 1) // self.block
+        else:  # one explicit boundary list shared by every unit, cut at chunk starts
+            from .chunking import check_boundaries
+
+            gb = check_boundaries(bounds, self.total_prompt)
+            c0, c1 = shard_chunks(gb, self.world)[self.rank]
+            self.lo, self.hi = gb[c0], gb[c1]
+            self.local_bounds = [x - self.lo for x in gb[c0:c1 + 1]]
+            n_total = len(gb) - 1
+            max_chunks = c1 - c0
         self.owns_tail = self.rank == self.world - 1
         self.local_len = self.hi - self.lo
         if self.local_len < 1:
@@ -109,14 +152,17 @@ class SplitKVShard:
         self.dec = SparseDecoder(batch, q_heads, kv_heads, head_dim, cap_len, block=block,
                                  top_k=top_k, budget=budget, dtype=torch.bfloat16, agg=agg,
                                  tile=tile, splits=splits, device=device, scoring="sketch",
-                                 attn_mode=attn_mode)
+                                 attn_mode=attn_mode, max_chunks=max_chunks)
         d = self.dec
         self.B, self.Hq, self.Hkv, self.D, self.G = d.B, d.Hq, d.Hkv, d.D, d.G
         self.budget = d.budget
-        self.spec = ShardSpec(self.lo // self.block,
-                              (self.total_prompt + self.block - 1) // self.block,
-                              self.total_prompt, 1 if self.owns_tail else 0)
-        self.cap = candidate_capacity(self.budget, self.block)
+        self.spec = ShardSpec(c0, n_total, self.total_prompt, 1 if self.owns_tail else 0)
+        if bounds is None:
+            self.cap = candidate_capacity(self.budget, self.block)
+        else:  # equal on every rank: the exchanged rows share one stride
+            self.cap = max(candidate_capacity(self.budget, self.block,
+                                              [gb[c + 1] - gb[c] for c in range(a, z)])
+                           for a, z in shard_chunks(gb, self.world))
         self.cand_stride = REC_BYTES * (self.cap + 1)
         kw = dict(device=d.dev)
         self.cand = torch.zeros(d.items * self.cand_stride, dtype=torch.uint8, **kw)
@@ -131,7 +177,7 @@ class SplitKVShard:
         """keys/values: this shard's prompt slice [B, Hkv, hi-lo, D] (bf16)."""
         if keys.shape[2] != self.local_len:
             raise ValueError(f"shard {self.rank} expects {self.local_len} prompt tokens")
-        self.dec.prefill(keys, values)
+        self.dec.prefill(keys, values, bounds=self.local_bounds)
 
     @property
     def items_per_unit(self):
@@ -212,7 +258,8 @@ class SplitKVShard:
         """Algorithmic HBM bytes of this shard's step (sketch + selected K/V +
         q/o + candidate/record exchange buffers)."""
         d = self.dec
-        nc = (self.local_len + self.block - 1) // self.block
+        nc = ((self.local_len + self.block - 1) // self.block if self.local_bounds is None
+              else len(self.local_bounds) - 1)
         return {"sketch": d.U * nc * d.D * 2,
                 "exchange": (self.cand.numel() + self.rec.numel() * 4) * self.world}
 

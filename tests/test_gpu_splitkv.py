@@ -15,7 +15,8 @@ from oracle import dhsa_oracle as O
 pytestmark = pytest.mark.gpu
 
 
-def _run(W, B, Hq, Hkv, D, P, steps, top_k, agg, kind="normal", seed=0, budget=None):
+def _run(W, B, Hq, Hkv, D, P, steps, top_k, agg, kind="normal", seed=0, budget=None,
+         bounds=None):
     from paper_2510_24606_b200.splitkv import SplitKVGroup
 
     t, host = make_inputs(B, Hq, Hkv, D, P, steps, torch.bfloat16, seed=seed, kind=kind)
@@ -23,11 +24,12 @@ def _run(W, B, Hq, Hkv, D, P, steps, top_k, agg, kind="normal", seed=0, budget=N
         t["k"][:, :, P - 64:P] = t["k"][:, :, 0:64]
         host["k"] = t["k"].to(torch.float64).numpy()
     grp = SplitKVGroup(B, Hq, Hkv, D, P, W, block=64, top_k=top_k, budget=budget, agg=agg,
-                       max_new=steps + 1)
+                       max_new=steps + 1, bounds=bounds)
     grp.prefill(t["k"][:, :, :P].cuda(), t["v"][:, :, :P].cuda())
     G = Hq // Hkv
     budget = grp.shards[0].budget
-    bounds = O.static_grid(P, 64)
+    if bounds is None:
+        bounds = O.static_grid(P, 64)
     oracles = {}
     for u in range(B * Hkv):
         b, h = divmod(u, Hkv)
@@ -97,4 +99,34 @@ def test_splitkv_ragged_prompt():
     """Prompt length not a multiple of the block: the last shard's last chunk
     is short; 3 shards."""
     worst = _run(3, B=1, Hq=4, Hkv=1, D=128, P=3001, steps=3, top_k=5, agg="max", seed=9)
+    assert worst <= TOL[torch.bfloat16], worst
+
+
+def _dyn_bounds(seed, P):
+    rng = np.random.default_rng(seed)
+    b, pos = [0], 0
+    while pos < P:
+        pos = min(P, pos + int(rng.choice([int(rng.integers(1, 64)), int(rng.integers(64, 400))])))
+        b.append(pos)
+    return b
+
+
+@pytest.mark.parametrize("W", [1, 2, 3])
+def test_splitkv_dynamic_chunks(W):
+    """Explicit boundary list (1..400-token chunks) cut at chunk starts over
+    W shards: the global walk over candidates of any length equals the
+    unsharded walk."""
+    P = 3000
+    worst = _run(W, B=1, Hq=8, Hkv=2, D=128, P=P, steps=3, top_k=8, agg="max", seed=W,
+                 bounds=_dyn_bounds(W, P))
+    assert worst <= TOL[torch.bfloat16], worst
+
+
+def test_splitkv_dynamic_small_budget_many_chunks():
+    """Many short chunks: the candidate capacity bound from the local chunk
+    lengths (shortest chunks first) holds."""
+    P = 1200
+    b = list(range(0, 600, 5)) + list(range(600, 1200, 97)) + [1200]
+    worst = _run(2, B=1, Hq=4, Hkv=1, D=128, P=P, steps=3, top_k=1, agg="max", budget=130,
+                 seed=4, bounds=b)
     assert worst <= TOL[torch.bfloat16], worst

@@ -247,3 +247,31 @@ def test_wire_formats_byte_identical(tmp_path):
     (tmp_path / "bad.msk").write_bytes(b"NOTAMASK")
     with pytest.raises(ValueError):
         S.load_mask(tmp_path / "bad.msk")
+
+
+def test_splitkv_dynamic_host_helpers():
+    """shard_chunks cuts at chunk starts (>= 1 chunk per shard, near-even
+    tokens); candidate_capacity(lengths) bounds the chunks a local walk
+    touches (oracle chunk_takes) for random lengths, scores and budgets."""
+    from oracle import dhsa_oracle as O
+    from paper_2510_24606_b200.splitkv import candidate_capacity, shard_chunks
+
+    rng = np.random.default_rng(0)
+    for _ in range(200):
+        n = int(rng.integers(1, 80))
+        lens = rng.integers(1, 300, size=n)
+        b = [0] + np.cumsum(lens).tolist()
+        W = int(rng.integers(1, min(n, 8) + 1))
+        cuts = shard_chunks(b, W)
+        assert cuts[0][0] == 0 and cuts[-1][1] == n
+        assert all(c0 < c1 for c0, c1 in cuts)
+        assert all(cuts[r][1] == cuts[r + 1][0] for r in range(W - 1))
+        budget = int(rng.integers(1, 3000))
+        cap = candidate_capacity(budget, 64, lens)
+        scores = rng.standard_normal(n)
+        if rng.random() < 0.3:
+            scores = np.round(scores)  # ties
+        takes = O.chunk_takes(scores, np.arange(n), lens, budget - 1)
+        assert int((takes > 0).sum()) + 1 <= cap  # + the generated chunk
+    with pytest.raises(ValueError):
+        shard_chunks([0, 5, 9], 3)

@@ -28,48 +28,62 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _problem(seed, P, D, g, block):
+def _dyn_bounds(rng, P):
+    b, pos = [0], 0
+    while pos < P:
+        pos = min(P, pos + int(rng.choice([int(rng.integers(1, 64)), int(rng.integers(64, 300))])))
+        b.append(pos)
+    return b
+
+
+def _problem(seed, P, D, g, block, dyn=False):
     rng = np.random.default_rng(seed)
     K = rng.standard_normal((P + g + 1, D))
     V = rng.standard_normal((P + g + 1, D))
     q = rng.standard_normal(D)
     if seed % 2:  # exact ties across shard borders: duplicated first/last blocks
         K[P - block:P] = K[0:block]
-    bounds = O.static_grid(P, block)
+    bounds = _dyn_bounds(rng, P) if dyn else O.static_grid(P, block)
     cached = O.centroids(K[:P], bounds)
     gen_sum = K[P:P + g].sum(axis=0) if g else np.zeros(D)
     s = O.decode_scores(q, cached, gen_sum, g, K[P + g])
     nc = len(bounds) - 1
     lens = np.diff(bounds).tolist() + ([g] if g else [])
     los = bounds[:-1] + ([P] if g else [])
-    return K, V, q, s[: nc + (1 if g else 0)], np.array(lens), np.array(los), nc
+    return K, V, q, s[: nc + (1 if g else 0)], np.array(lens), np.array(los), nc, bounds
 
 
-def _worker(rank, world, port, seed):
+def _worker(rank, world, port, seed, dyn=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2510_24606_b200.splitkv import (REC_BYTES, TorchComm, candidate_capacity,
-                                                    shard_ranges)
+                                                    shard_chunks, shard_ranges)
 
         assert REC.itemsize == REC_BYTES
         comm = TorchComm()
         P, D, g, block, budget = 1900, 32, 5, 64, 300
-        K, V, q, s, lens, los, nc = _problem(seed, P, D, g, block)
+        K, V, q, s, lens, los, nc, bounds = _problem(seed, P, D, g, block, dyn)
         row = P + g
         R = min(budget, row + 1) - 1
         ids = np.arange(len(s))
         full_takes = O.chunk_takes(s, ids, lens, R)
 
-        lo, hi = shard_ranges(P, block, world)[rank]
+        if dyn:  # the product's cut (chunk starts) and rank-uniform capacity
+            cuts = shard_chunks(bounds, world)
+            lo, hi = bounds[cuts[rank][0]], bounds[cuts[rank][1]]
+            cap = max(candidate_capacity(budget, block, np.diff(bounds)[a:z]) for a, z in cuts)
+        else:
+            lo, hi = shard_ranges(P, block, world)[rank]
+            cap = candidate_capacity(budget, block)
         mine = [c for c in range(nc) if lo <= los[c] < hi]
         if rank == world - 1 and g:
             mine.append(nc)  # the generated chunk lives on the tail shard
         mine = np.array(mine, dtype=np.int64)
         local = mine[O.split_candidates(s[mine], ids[mine], lens[mine], R)]
 
-        cap = candidate_capacity(budget, block)
+        assert len(local) <= cap
         rowbuf = np.zeros(cap + 1, dtype=REC)
         rowbuf[0]["gid"] = len(local)  # header: count in the first record's first int
         hdr = rowbuf.view(np.uint8)[:4].view(np.int32)
@@ -116,6 +130,12 @@ def _worker(rank, world, port, seed):
 @pytest.mark.parametrize("world,seed", [(2, 0), (2, 1), (3, 2), (3, 3)])
 def test_splitkv_exchange_gloo(world, seed):
     mp.spawn(_worker, args=(world, _free_port(), seed), nprocs=world, join=True)
+
+
+@pytest.mark.parametrize("world,seed", [(2, 4), (3, 5)])
+def test_splitkv_exchange_gloo_dynamic_chunks(world, seed):
+    """Explicit boundary list (1..300-token chunks) cut at chunk starts."""
+    mp.spawn(_worker, args=(world, _free_port(), seed, True), nprocs=world, join=True)
 
 
 def test_shard_ranges_cover_prompt():
