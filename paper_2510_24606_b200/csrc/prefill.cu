@@ -303,6 +303,81 @@ __device__ __forceinline__ float exp2_mufu(float x) {
   return y;
 }
 
+// Blackwell packed fp32 pairs (FFMA2 / FADD2): half the issue slots of the
+// scalar forms in the softmax, which is issue-bound.
+__device__ __forceinline__ uint64_t f2_u64(float a, float b) {
+  return (uint64_t)__float_as_uint(a) | ((uint64_t)__float_as_uint(b) << 32);
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ float lo_f(uint64_t x) { return __uint_as_float((uint32_t)x); }
+__device__ __forceinline__ float hi_f(uint64_t x) { return __uint_as_float((uint32_t)(x >> 32)); }
+
+// max over 64 raw scores: four independent FMNMX3 chains instead of one
+__device__ __forceinline__ float row_max64(const uint32_t* v) {
+  float m[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+  for (int c = 0; c < 64; c += 8)
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      m[k] = fmaxf(m[k], fmaxf(__uint_as_float(v[c + 2 * k]), __uint_as_float(v[c + 2 * k + 1])));
+  return fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3]));
+}
+
+#ifndef DHSA_POLY_PAIRS
+#define DHSA_POLY_PAIRS 0  // pairs (of every 8) whose exp2 runs on the FMA pipe;
+#endif                      // measured slower at 2..4 (-8..-14% TFLOP/s): not MUFU-bound
+
+// 2^x for a pair on the FMA pipe (the MUFU pipe is shared by both M tiles'
+// softmax warps): round-to-nearest split x = n + f, |f| <= 1/2, degree-3
+// polynomial (max rel. error 7.8e-5, below bf16's 3.9e-3), n added to the
+// exponent field.  x is clamped at -125 (masked -inf columns give ~2^-125,
+// negligible against the row max term 1).
+__device__ __forceinline__ void exp2_poly2(uint64_t x, float& p0, float& p1) {
+  const float x0 = fmaxf(lo_f(x), -125.f), x1 = fmaxf(hi_f(x), -125.f);
+  const uint64_t magic = f2_u64(12582912.f, 12582912.f);  // 1.5 * 2^23
+  const uint64_t t = fadd2(f2_u64(x0, x1), magic);        // n in the low mantissa bits
+  const uint64_t n = fadd2(t, f2_u64(-12582912.f, -12582912.f));
+  const uint64_t f = fadd2(f2_u64(x0, x1), n ^ 0x8000000080000000ull);  // x - n
+  uint64_t r = ffma2(f, f2_u64(0.05508876591920853f, 0.05508876591920853f),
+                     f2_u64(0.24260465800762177f, 0.24260465800762177f));
+  r = ffma2(r, f, f2_u64(0.6932762861251831f, 0.6932762861251831f));
+  r = ffma2(r, f, f2_u64(0.999928891658783f, 0.999928891658783f));
+  p0 = __uint_as_float((uint32_t)r + ((uint32_t)t << 23));
+  p1 = __uint_as_float((uint32_t)(r >> 32) + ((uint32_t)(t >> 32) << 23));
+}
+
+// p = 2^(s * sl2 - mref) for 64 scores, packed to bf16 pairs in pk; returns
+// the sum of the p (two packed accumulators)
+__device__ __forceinline__ float softmax_pack64(const uint32_t* v, float sl2, float mref,
+                                                uint32_t* pk) {
+  const uint64_t sc2 = f2_u64(sl2, sl2), nm2 = f2_u64(-mref, -mref);
+  uint64_t acc[2] = {0ull, 0ull};
+#pragma unroll
+  for (int t = 0; t < 32; ++t) {
+    const uint64_t x = ffma2((uint64_t)v[2 * t] | ((uint64_t)v[2 * t + 1] << 32), sc2, nm2);
+    float p0, p1;
+    if ((t & 7) < DHSA_POLY_PAIRS) {
+      exp2_poly2(x, p0, p1);
+    } else {
+      p0 = exp2_mufu(lo_f(x));
+      p1 = exp2_mufu(hi_f(x));
+    }
+    acc[t & 1] = fadd2(acc[t & 1], f2_u64(p0, p1));
+    pk[t] = pack_bf16(p0, p1);
+  }
+  const uint64_t a = fadd2(acc[0], acc[1]);
+  return lo_f(a) + hi_f(a);
+}
+
 // D[tmem] (+)= A[tmem] * B[smem] (A = P in TMEM, K-major; "TS" form).
 __device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
                                              uint32_t idesc, uint32_t accumulate) {
@@ -481,17 +556,12 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_kernel(
       tmem_ld32(tS + (j & 1) * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
       tmem_wait_ld();
       // raw max (the scale is positive); masking only where some row needs it
-      float mx = -INFINITY;
-      if (__all_sync(0xffffffffu, lim == 64 && self < 0)) {
+      if (!__all_sync(0xffffffffu, lim == 64 && self < 0)) {
 #pragma unroll
-        for (int c = 0; c < 64; ++c) mx = fmaxf(mx, __uint_as_float(v[c]));
-      } else {
-#pragma unroll
-        for (int c = 0; c < 64; ++c) {
+        for (int c = 0; c < 64; ++c)
           if (!(c < lim || c == self)) v[c] = __float_as_uint(-INFINITY);
-          mx = fmaxf(mx, __uint_as_float(v[c]));
-        }
       }
+      float mx = row_max64(v);
       mx *= sl2;
       // lazy rescale: a row moves its reference max only when its running max
       // grows by > 2^8 (or on its first finite score, when O holds only
@@ -523,13 +593,7 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_kernel(
       // p = 2^(s*scale - m) on MUFU (a polynomial on the FMA pipe for part of
       // the columns measured slower: the softmax is issue-bound, not MUFU-bound)
       uint32_t pk[32];
-#pragma unroll
-      for (int t = 0; t < 32; ++t) {
-        const float p0 = exp2_mufu(fmaf(__uint_as_float(v[2 * t]), sl2, -mref));
-        const float p1 = exp2_mufu(fmaf(__uint_as_float(v[2 * t + 1]), sl2, -mref));
-        lsum += p0 + p1;
-        pk[t] = pack_bf16(p0, p1);
-      }
+      lsum += softmax_pack64(v, sl2, mref, pk);
       tmem_st32(tS + (j & 1) * 64, pk);  // P over the first 32 columns of its S buffer
       tmem_wait_st();
       tc_fence_before();
@@ -807,17 +871,12 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_persist_kernel(
         tmem_ld32(tS + (jj & 1) * 64, *reinterpret_cast<uint32_t(*)[32]>(v));
         tmem_ld32(tS + (jj & 1) * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
         tmem_wait_ld();
-        float mx = -INFINITY;
-        if (__all_sync(0xffffffffu, lim == 64 && self < 0)) {
+        if (!__all_sync(0xffffffffu, lim == 64 && self < 0)) {
 #pragma unroll
-          for (int c = 0; c < 64; ++c) mx = fmaxf(mx, __uint_as_float(v[c]));
-        } else {
-#pragma unroll
-          for (int c = 0; c < 64; ++c) {
+          for (int c = 0; c < 64; ++c)
             if (!(c < lim || c == self)) v[c] = __float_as_uint(-INFINITY);
-            mx = fmaxf(mx, __uint_as_float(v[c]));
-          }
         }
+        float mx = row_max64(v);
         mx *= sl2;
         float m_new = m_used;
         if (mx > -INFINITY && (m_used == -INFINITY || mx > m_used + 8.f)) m_new = mx;
@@ -841,13 +900,7 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_persist_kernel(
         m_used = m_new;
         const float mref = m_used == -INFINITY ? 0.f : m_used;
         uint32_t pk[32];
-#pragma unroll
-        for (int t = 0; t < 32; ++t) {
-          const float p0 = exp2_mufu(fmaf(__uint_as_float(v[2 * t]), sl2, -mref));
-          const float p1 = exp2_mufu(fmaf(__uint_as_float(v[2 * t + 1]), sl2, -mref));
-          lsum += p0 + p1;
-          pk[t] = pack_bf16(p0, p1);
-        }
+        lsum += softmax_pack64(v, sl2, mref, pk);
         tmem_st32(tS + (jj & 1) * 64, pk);
         tmem_wait_st();
         tc_fence_before();
