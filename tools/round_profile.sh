@@ -12,7 +12,9 @@ timeout 600 python -m pytest tests -m gpu -q > $out/gpu_tests.log 2>&1; tail -3 
 timeout 600 python bench.py > $out/bench_c3.json 2> $out/bench_c3.err; tail -c 400 $out/bench_c3.json
 timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > $out/bench_ref.json 2> $out/bench_ref.err
 timeout 300 python bench.py --config C4 --steps 20 --warmup 5 > $out/bench_c4.json 2> $out/bench_c4.err
-timeout 300 python bench.py --config C5 --steps 5 --warmup 3 > $out/bench_c5.json 2> $out/bench_c5.err
+timeout 600 python bench.py --config C5 --steps 5 --warmup 3 > $out/bench_c5.json 2> $out/bench_c5.err
+timeout 300 python bench.py --config C2 --steps 50 --warmup 5 > $out/bench_c2.json 2> $out/bench_c2.err
+timeout 300 python bench.py --config C1 --steps 50 --warmup 5 > $out/bench_c1.json 2> $out/bench_c1.err
 SMALL="--steps 2 --warmup 3 --roll-steps 0 --breakdown-steps 2 --e2e-steps 2 --no-cpu"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file $out/launches_c3.csv python bench.py $SMALL > /dev/null 2>&1
@@ -21,7 +23,9 @@ timeout 900 ncu --set full --clock-control none --import-source on \
   -o $out/prof_c3 -f python bench.py $SMALL > $out/ncu_c3.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on \
   -k regex:"prefill_attn_kernel|prefill_plan_kernel|prefill_scores_kernel" -s 3 -c 3 \
-  -o $out/prof_c5 -f python bench.py --config C5 --c5-topk 64 --steps 1 --warmup 1 > $out/ncu_c5.log 2>&1
+  -o $out/prof_c5 -f python bench.py --config C5 --c5-topk 64 --steps 1 --warmup 1 --no-quality \
+  --no-dynamic > $out/ncu_c5.log 2>&1
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-  --log-file $out/launches_c5.csv python bench.py --config C5 --c5-topk 64 --steps 1 --warmup 1 > /dev/null 2>&1
+  --log-file $out/launches_c5.csv python bench.py --config C5 --c5-topk 64 --steps 1 --warmup 1 \
+  --no-quality --no-dynamic > /dev/null 2>&1
 ls -la $out
