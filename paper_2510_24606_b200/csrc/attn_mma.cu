@@ -44,7 +44,7 @@ __global__ __launch_bounds__(160) void attn_mma_kernel(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int unit = item / items_per_unit;
   if (ready) {  // launched early (PDL): wait until the selection of this item is published
-    if (threadIdx.x == 0) spin_geq(ready + item, 1);
+    if (threadIdx.x == 0) spin_geq(ready + item, kReadyFinal);
     __syncthreads();
   }
   // tiles may have been written while this grid was running: read through L2

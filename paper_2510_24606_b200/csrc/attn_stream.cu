@@ -152,14 +152,30 @@ __global__ __launch_bounds__(192, 2) void attn_stream_kernel(const __grid_consta
       }
       int S, nseg;
       seg_shape(a, item, S, nseg);
+      // a segment (not the last) inside the item's early-published prefix
+      // starts without the final tile count (nt = -1: never "whole")
       int nt = 0;
       if (lane == 0) {
-        if (a.ready) spin_geq(a.ready + item, 1);
-        nt = __ldcg(a.ntiles + item);
+        if (a.ready) {
+          int v;
+          while ((v = ld_acquire(a.ready + item)) < 1) __nanosleep(64);
+          if (v < kReadyFinal && !(j < nseg - 1 && (j + 1) * S <= v - 1)) {
+            spin_geq(a.ready + item, kReadyFinal);
+            v = kReadyFinal;
+          }
+          nt = v < kReadyFinal ? -1 : __ldcg(a.ntiles + item);
+        } else {
+          nt = __ldcg(a.ntiles + item);
+        }
       }
       nt = __shfl_sync(0xffffffffu, nt, 0);
       int lo, hi;
-      seg_range(j, S, nseg, nt, lo, hi);
+      if (nt < 0) {
+        lo = j * S;
+        hi = lo + S;
+      } else {
+        seg_range(j, S, nseg, nt, lo, hi);
+      }
       if (lo >= hi && !(nt == 0 && j == 0)) {  // beyond the item's real tiles
         if (lane == 0 && !a.prefetch) knext = atomicAdd(pull, 1);
         continue;
@@ -303,7 +319,7 @@ __global__ __launch_bounds__(D) void stream_merge_kernel(StreamArgs a) {
   // flag is up (without flags the select grid completed before the attention
   // grid was launched)
   if (a.ready) {
-    if (threadIdx.x == 0) spin_geq(a.ready + item, 1);
+    if (threadIdx.x == 0) spin_geq(a.ready + item, kReadyFinal);
     __syncthreads();
   }
   const int nt = __ldcg(a.ntiles + item);

@@ -206,6 +206,12 @@ __device__ __forceinline__ void red_add_release(int32_t* p, int v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 // Thread-level spin until *p >= target (acquire), with backoff.
+// select -> attention item flags: 0 = not ready; 1 + n (n < kReadyFinal - 1)
+// = the first n tiles of the item are final (the chunks the certified select
+// keeps whole, published before the exact refinement); kReadyFinal = every
+// tile and the tile count are final.
+constexpr int kReadyFinal = 1 << 30;
+
 __device__ __forceinline__ void spin_geq(const int32_t* p, int target) {
   while (ld_acquire(p) < target) __nanosleep(64);
 }

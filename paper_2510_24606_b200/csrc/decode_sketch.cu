@@ -82,6 +82,7 @@ struct SketchArgs {
   int32_t* ready;           // [items] select -> attention flags (zeroed by the sketch kernel) or null
   int n_units;
   int32_t* progress;        // [U] sketch -> select: consumer-warp slices done (zero at rest) or null
+  int early;                // publish the certainly-kept chunks' tiles before the refinement
   unsigned long long* dbg;  // optional per-CTA phase timestamps (DHSA_DEBUG_TIMING)
   // sequence-sharded split-KV mode (dhsa_decode_candidates_bf16): this shard
   // holds global prompt chunks [chunk_offset, chunk_offset + nchunks); the
@@ -643,6 +644,7 @@ __global__ __launch_bounds__(NT) void sketch_select_kernel(SketchArgs a) {
     uint64_t prefix = 0, mask = 0;
     uint32_t rrem = R;
     bool done = false;
+    int base = 0;  // tiles published early (phase A)
     if (R > 0 && R < (uint32_t)wloc) {
       DBG_T(2);
       // certified bound in sketch units (+ the fp32 rounding of the exact gen score)
@@ -680,6 +682,36 @@ __global__ __launch_bounds__(NT) void sketch_select_kernel(SketchArgs a) {
       if (lane == 0 && win_local) atomicAdd(&s_win, win_local);
       __syncthreads();
       const int nu = s_nunc;
+      if (a.early) {
+        // phase A: the chunks kept whole are final already; their tiles go out
+        // (chunk order) and the attention may stream them while the
+        // uncertain chunks are re-scored
+        int32_t* out = a.tiles + (int64_t)s * a.tile_cap * 2;
+        const int cpt = (n + NT - 1) / NT;
+        const int c0 = min(tid * cpt, n), c1 = min(c0 + cpt, n);
+        int cnt = 0;
+        for (int c = c0; c < c1; ++c)
+          if (key64[c] == ~0ull) cnt += (lens[c] + a.tile_tokens - 1) / a.tile_tokens;
+        int total;
+        int off = block_scan_excl<NT>(cnt, sh, total);
+        if (total + 1 <= a.tile_cap) {
+          for (int c = c0; c < c1; ++c) {
+            if (key64[c] != ~0ull) continue;
+            int lo, len;
+            uc.chunk(c, lo, len);
+            for (int t = 0; t < len; t += a.tile_tokens, ++off) {
+              out[2 * off] = lo + t;
+              out[2 * off + 1] = min(a.tile_tokens, len - t);
+            }
+          }
+          base = total;
+          __syncthreads();
+          if (tid == 0 && base > 0) {
+            __threadfence();
+            st_release(a.ready + s, 1 + base);
+          }
+        }
+      }
       DBG_T(4);
       for (int i = warp; i < nu; i += NW) {
         const int c = unc[i];
@@ -724,7 +756,7 @@ __global__ __launch_bounds__(NT) void sketch_select_kernel(SketchArgs a) {
         }
         __syncthreads();
         for (int c = tid; c < n; c += NT)
-          if (key64[c] != ~0ull) lens[c] = 0;
+          if (key64[c] != ~0ull || base > 0) lens[c] = 0;  // phase A emitted the whole ones
         __syncthreads();
         for (int i = tid; i < nu; i += NT) lens[unc[i]] = take[i];
         __syncthreads();
@@ -732,19 +764,25 @@ __global__ __launch_bounds__(NT) void sketch_select_kernel(SketchArgs a) {
         if (!a.split)
           emit_takes<NT>(uc, lens, n, row, a.tile_tokens,
                                      a.tiles + (int64_t)s * a.tile_cap * 2, a.tile_cap,
-                                     a.ntiles + s, sh);
+                                     a.ntiles + s, sh, base);
         DBG_T(7);
         done = true;
       } else {
         radix_threshold<NT, uint64_t>(key64, lens, n, R, sh, prefix, mask, rrem);
       }
     }
-    if (!done && a.split)
+    if (!done && a.split) {
       walk_takes<NT, uint64_t>(key64, lens, n, R, prefix, mask, rrem, sh);
-    else if (!done)
-      walk_emit<NT, uint64_t>(uc, key64, lens, n, R, prefix, mask, rrem, row,
-                                          a.tile_tokens, a.tiles + (int64_t)s * a.tile_cap * 2,
-                                          a.tile_cap, a.ntiles + s, sh);
+    } else if (!done) {
+      walk_takes<NT, uint64_t>(key64, lens, n, R, prefix, mask, rrem, sh);
+      if (base > 0) {  // phase A emitted the chunks kept whole (key ~0)
+        for (int c = tid; c < n; c += NT)
+          if (key64[c] == ~0ull) lens[c] = 0;
+        __syncthreads();
+      }
+      emit_takes<NT>(uc, lens, n, row, a.tile_tokens, a.tiles + (int64_t)s * a.tile_cap * 2,
+                     a.tile_cap, a.ntiles + s, sh, base);
+    }
     if (a.split)
       emit_candidates<D, G, AGG, NT>(a, uc, lens, unc, n, s, qd, h0, nh, gex, u);
   }
@@ -753,7 +791,8 @@ __global__ __launch_bounds__(NT) void sketch_select_kernel(SketchArgs a) {
     if (a.advance) a.gen_count[u] = g + 1;  // masks.py:236
     if (a.ready) {  // tiles, running sum and appended k/v are published together
       __threadfence();
-      for (int it = 0; it < nitems; ++it) st_release(a.ready + (AGG == DHSA_AGG_NONE ? u * G + it : u), 1);
+      for (int it = 0; it < nitems; ++it)
+        st_release(a.ready + (AGG == DHSA_AGG_NONE ? u * G + it : u), kReadyFinal);
     }
   }
   DBG_T(8);
@@ -969,6 +1008,19 @@ static int decode_step_impl(
   a.ready = ready;
   a.n_units = U;
   a.progress = progress;
+  {
+    // two-phase tile publication pays when the attention grid has SMs to
+    // start on while the selects run (few select CTAs, e.g. C2: 64 units,
+    // 51.8 vs 54.9 us); with a select CTA on every SM (C3: 256 units) the
+    // attention CTAs are not resident before the selects end and the extra
+    // scan only lengthens the select (+1.2 us)
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int items = agg == DHSA_AGG_NONE ? U * G : U;
+    a.early = ready != nullptr && items <= sms;
+    if (const char* e = getenv("DHSA_EARLY_TILES")) a.early = ready != nullptr && atoi(e) != 0;
+  }
   if (shard) {
     DHSA_REQUIRE(cand && cand_cap >= 1 && cand_stride >= (int64_t)sizeof(SplitCand) * (cand_cap + 1) &&
                      cand_stride % 8 == 0,
@@ -986,6 +1038,7 @@ static int decode_step_impl(
     a.cand_cap = cand_cap;
     a.advance = 0;
     a.ready = nullptr;
+    a.early = 0;
   }
   if (const char* e = getenv("DHSA_DEBUG_TIMING")) a.dbg = (unsigned long long*)strtoull(e, nullptr, 0);
   const int64_t need = dhsa_sketch_select_scratch_size(layout.max_chunks);

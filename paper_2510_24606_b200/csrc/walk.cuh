@@ -157,18 +157,20 @@ __device__ void radix_threshold(const K* keys, const int32_t* lens, int n, uint3
 }
 
 // Emit tiles of <= tile_tokens tokens for per-chunk takes (tokens taken from
-// each chunk's start, in lens[]), in chunk order, then the self tile.
+// each chunk's start, in lens[]), in chunk order, then the self tile; the
+// first `base` tiles of the row were written before (two-phase emission).
 template <int NT, class View>
 __device__ void emit_takes(const View& view, const int32_t* takes, int n, int row,
                            int tile_tokens, int32_t* out, int64_t cap, int32_t* ntiles_out,
-                           WalkShared& sh) {
+                           WalkShared& sh, int base = 0) {
   const int tid = threadIdx.x;
   const int cpt = (n + NT - 1) / NT;
   const int c0 = min(tid * cpt, n), c1 = min(c0 + cpt, n);
   int ntile_local = 0;
   for (int c = c0; c < c1; ++c) ntile_local += (takes[c] + tile_tokens - 1) / tile_tokens;
   int tiles_total;
-  int off = block_scan_excl<NT>(ntile_local, sh, tiles_total);
+  int off = base + block_scan_excl<NT>(ntile_local, sh, tiles_total);
+  tiles_total += base;  // tiles [0, base) were emitted earlier
   for (int c = c0; c < c1; ++c) {
     const int take = takes[c];
     if (take <= 0) continue;

@@ -142,7 +142,7 @@ def test_step_graph_replay_matches_eager():
 @pytest.mark.parametrize("agg", ["max", "mean", "none"])
 @pytest.mark.parametrize("kind", ["normal", "ties", "int", "outlier", "zeroq"])
 def test_sketch_scoring_equals_fp64_scoring(agg, kind):
-    """The bf16-sketch + certified-refinement selection is index-identical to
+    """The bf16-sketch + certified-refinement selection is token-identical to
     streaming the fp64 centroids, including exact ties (duplicated blocks,
     integer data), an outlier chunk whose norm inflates the error bound, and
     an all-zero query (every score ties)."""
@@ -167,8 +167,12 @@ def test_sketch_scoring_equals_fp64_scoring(agg, kind):
         sels.append(per)
     for (sa, oa), (sb, ob) in zip(*sels):
         for a, b in zip(sa, sb):
-            assert np.array_equal(a, b)
-        assert torch.equal(oa, ob)
+            assert np.array_equal(tiles_to_idx(a), tiles_to_idx(b))
+        # the sketch path emits the certainly-kept chunks' tiles first (the
+        # attention starts on them early), so the fp32 partial sums are
+        # grouped differently: equal up to bf16 rounding
+        oa, ob = oa.float(), ob.float()
+        assert (oa - ob).abs().max() <= 1e-2 * ob.abs().max()
 
 
 def test_sketch_c3_shape_sampled_units():
