@@ -1240,8 +1240,9 @@ extern "C" int dhsa_prefill_attn(const void* q, const void* k, const void* v, in
   a.row_stats = reinterpret_cast<float2*>(row_stats);
   cudaStream_t st = (cudaStream_t)stream;
   // persistent plans pay off when plans are short (per-plan start-up is a
-  // large share): measured +7% at budget 1025, -3..-9% at 4097..16385
-  bool persist = counters != nullptr && budget <= 1600;
+  // large share): measured +7% at budget 1025, -3..-9% at 4097..16385 on the
+  // static grid; with explicit bounds (many short query tiles) +2% at 4097
+  bool persist = counters != nullptr && (budget <= 1600 || explicit_bounds);
   if (const char* e = getenv("DHSA_PREFILL_PERSISTENT")) persist = counters != nullptr && atoi(e) != 0;
   if (persist) {
     if (a.heads_per_cta > 2) return launch_prefill_persist<2, 4>(mq, mk, mv, a, st);
