@@ -121,7 +121,7 @@ class BoundaryPredictor:
                 f"need at least {2 * pr.window + 1} keys, got shape {tuple(keys.shape)}")
         if keys.shape[1] != pr.dim:
             raise ValueError(f"keys have dim {keys.shape[1]}, predictor expects {pr.dim}")
-        keys = keys.to(torch.float64).contiguous()
+        keys = keys.to(device=_dev.device(), dtype=torch.float64).contiguous()
         L = keys.shape[0]
         lib = _lib.load()
         nbytes = lib.dhsa_predictor_workspace_size(L, pr.dim, pr.window, pr.hidden)
