@@ -102,6 +102,8 @@ class SparsePrefill:
         shared = not per_unit
         ncs = [len(b) - 1 for b in lists]
         nc = max(ncs)
+        if nc > 10240:  # plan-kernel shared memory (20 B per chunk) and the S x n x n scores
+            raise ValueError(f"{nc} chunks exceed the prefill limit of 10240 per unit")
         # worst-case plan entries: blocks of the chunks a walk of budget-1
         # tokens can touch (the most chunks: the shortest ones), + the diagonal
         cap = 2
