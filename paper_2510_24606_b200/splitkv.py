@@ -237,6 +237,11 @@ class SplitKVShard:
         """Enqueue one step on the current (or given) stream: 4 kernels + 2
         all-gathers; graph-capturable when the collective is."""
         self.candidates(q, k_new, v_new, stream)
+        if comm.world == 1:  # one shard: the gathered rows are this shard's own
+            self.select(self.cand, stream=stream)
+            self.attend(q, stream)
+            self.merge(out, self.rec, stream=stream)
+            return
         comm.all_gather(self.gathered, self.cand)
         self.select(stream=stream)
         self.attend(q, stream)
