@@ -288,3 +288,40 @@ def test_prefill_dynamic_mask_export():
     bits = pf.mask_bitsets().cpu().numpy()[0]
     rows = O.prefill_rows(host["q"][0], np.repeat(host["k"][0], 4, axis=0), bounds, 150)
     assert np.array_equal(bits, S.rows_to_bitsets(L, rows))
+
+
+def test_mask_quality_dynamic_bounds():
+    """Recall / cosine per row with an explicit boundary list."""
+    from paper_2510_24606_b200.prefill import SparsePrefill, mask_quality
+
+    rng = np.random.default_rng(17)
+    B, Hq, Hkv, L, D = 1, 4, 1, 700, 128
+    bounds = _rand_bounds(rng, L)
+    t, host = _inputs(B, Hq, Hkv, L, D, 92)
+    pf = SparsePrefill(B, Hq, Hkv, D, L, budget=150, agg="max", bounds=bounds)
+    rec, cos = mask_quality(t["q"].cuda(), t["k"].cuda(), t["v"].cuda(), pf)
+    rec, cos = rec.cpu().numpy(), cos.cpu().numpy()
+    kh = np.repeat(host["k"][0, 0][None], Hq, axis=0)
+    rows = O.prefill_rows(host["q"][0], kh, bounds, pf.budget)
+    for h in range(Hq):
+        r_ref, c_ref = O.mask_quality(host["q"][0, h], host["k"][0, 0], host["v"][0, 0], rows)
+        assert np.abs(rec[0, h] - r_ref).max() <= 1e-2
+        assert np.abs(cos[0, h] - c_ref).max() <= 1e-2
+
+
+def test_predictor_nms_prefill_pipeline():
+    """The paper's pipeline on the GPU: boundary predictor over each kv
+    head's keys (fp64) -> nms_boundaries -> per-unit chunk lists -> sparse
+    prefill; rows index-exact against the oracle on the same boundaries."""
+    from paper_2510_24606_b200.chunking import nms_boundaries
+    from paper_2510_24606_b200.predictor import boundary_scores, init_predictor
+
+    L, Hkv = 1200, 2
+    t, host = _inputs(1, 8, Hkv, L, 128, 23)
+    params = init_predictor(128, window=4, heads=8, hidden=64, seed=3)
+    bounds = [nms_boundaries(boundary_scores(host["k"][0, h], params), min_conf=0.05,
+                             window=16, max_chunks=40) for h in range(Hkv)]
+    assert all(len(b) > 3 for b in bounds)
+    worst = _run(B=1, Hq=8, Hkv=Hkv, L=L, budget=300, agg="max", seed=23, bounds=bounds,
+                 check_rows=range(0, L, 3))
+    assert worst <= TOL_BF16, worst
