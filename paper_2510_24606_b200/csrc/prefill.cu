@@ -111,6 +111,76 @@ __global__ __launch_bounds__(256) void prefill_scores_kernel(
     }
 }
 
+// K7 on the FP64 tensor cores (DMMA m8n8k4): the 64 x D K-centroid tile and
+// one head's 64 x D Q tile are staged in shared memory once (rows padded to
+// D + 4 doubles: 8 rows x 4 k of a fragment load cover all 32 banks twice),
+// each warp owns 8 query rows x 64 key chunks (8 accumulator tiles).
+__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+template <int D>
+__global__ __launch_bounds__(256) void prefill_scores_dmma_kernel(
+    const double* __restrict__ qc, const double* __restrict__ kc, int nc, int G, int per_head,
+    int agg, double* __restrict__ out) {
+  constexpr int P = D + 4;
+  extern __shared__ __align__(16) double sm[];
+  double* sk = sm;            // [64][P]
+  double* sq = sm + 64 * P;   // [64][P]
+  const int s = blockIdx.z;
+  const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
+  if (j0 > i0) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int u = per_head ? s / G : s;
+  const int nh = per_head ? 1 : G;
+  const int h0 = per_head ? s : s * G;
+  const double* K = kc + (int64_t)u * nc * D;
+  for (int e = threadIdx.x; e < 64 * D; e += 256) {
+    const int r = e / D, d = e - r * D;
+    sk[r * P + d] = j0 + r < nc ? K[(int64_t)(j0 + r) * D + d] : 0.0;
+  }
+  double res[8][2];
+  const int ar = warp * 8 + (lane >> 2), ak = lane & 3;  // A fragment: row, k
+  for (int j = 0; j < nh; ++j) {
+    const double* Q = qc + (int64_t)(h0 + j) * nc * D;
+    __syncthreads();  // previous head's sq reads done
+    for (int e = threadIdx.x; e < 64 * D; e += 256) {
+      const int r = e / D, d = e - r * D;
+      sq[r * P + d] = i0 + r < nc ? Q[(int64_t)(i0 + r) * D + d] : 0.0;
+    }
+    __syncthreads();
+    double acc[8][2];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) acc[t][0] = acc[t][1] = 0.0;
+#pragma unroll 4
+    for (int k0 = 0; k0 < D; k0 += 4) {
+      const double a = sq[ar * P + k0 + ak];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) dmma_8x8x4(acc[t], a, sk[(t * 8 + (lane >> 2)) * P + k0 + ak]);
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        if (j == 0) res[t][e] = acc[t][e];
+        else if (agg == DHSA_AGG_MAX) res[t][e] = fmax(res[t][e], acc[t][e]);
+        else res[t][e] = res[t][e] + acc[t][e];
+      }
+  }
+  const int ri = i0 + warp * 8 + (lane >> 2);
+#pragma unroll
+  for (int t = 0; t < 8; ++t)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      double v = res[t][e];
+      if (agg == DHSA_AGG_MEAN && nh > 1) v = v / (double)nh;
+      const int cj = j0 + t * 8 + 2 * (lane & 3) + e;
+      if (ri < nc && cj < nc) out[((int64_t)s * nc + ri) * nc + cj] = v;
+    }
+}
+
 // ------------------------------------------------------------------- K8 --
 constexpr int kPlanThreads = 128;
 constexpr int kTok = 64;  // KV block / query tile rows of the tcgen05 kernel
@@ -1150,6 +1220,20 @@ extern "C" int dhsa_prefill_scores(const double* q_centroids, const double* k_ce
   const int S = per_head ? U * G : U;
   const int t = (n_chunks + kScT - 1) / kScT;
   dim3 grid((unsigned)t, (unsigned)t, (unsigned)S);
+  bool dmma = D == 128;
+  if (const char* e = getenv("DHSA_SCORES_DMMA")) dmma = dmma && atoi(e) != 0;
+  if (dmma) {
+    constexpr int smem = 2 * 64 * (128 + 4) * 8;
+    cudaError_t e = cudaFuncSetAttribute(prefill_scores_dmma_kernel<128>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) {
+      set_error("dhsa_prefill_scores: %s", cudaGetErrorString(e));
+      return DHSA_ECUDA;
+    }
+    prefill_scores_dmma_kernel<128><<<grid, 256, smem, (cudaStream_t)stream>>>(
+        q_centroids, k_centroids, n_chunks, G, per_head, agg, scores);
+    return check_launch("dhsa_prefill_scores");
+  }
   prefill_scores_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(q_centroids, k_centroids, n_chunks,
                                                                  D, G, per_head, agg, scores);
   return check_launch("dhsa_prefill_scores");
