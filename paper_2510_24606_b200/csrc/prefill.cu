@@ -121,14 +121,36 @@ __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  const uint32_t d = smem_u32(dst);
+  const int n = valid ? 16 : 0;  // src-size 0: zero fill
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(n)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// 64 x D fp64 tile rows [r0, r0 + 64) of src (row stride D) -> smem rows of P
+// doubles, 16-byte cp.async (rows past nc zero-filled)
+template <int D, int P>
+__device__ __forceinline__ void load_tile_async(double* dst, const double* src, int r0, int nc) {
+  for (int e = threadIdx.x; e < 64 * D / 2; e += 256) {
+    const int r = e / (D / 2), d2 = e - r * (D / 2);
+    const bool ok = r0 + r < nc;
+    cp_async16(dst + r * P + 2 * d2, src + (int64_t)(ok ? r0 + r : r0) * D + 2 * d2, ok);
+  }
+  cp_async_commit();
+}
+
 template <int D>
 __global__ __launch_bounds__(256) void prefill_scores_dmma_kernel(
     const double* __restrict__ qc, const double* __restrict__ kc, int nc, int G, int per_head,
     int agg, double* __restrict__ out) {
   constexpr int P = D + 4;
   extern __shared__ __align__(16) double sm[];
-  double* sk = sm;            // [64][P]
-  double* sq = sm + 64 * P;   // [64][P]
+  double* sk = sm;                          // [64][P]
+  double* const sq0 = sm + 64 * P;          // double-buffered head tiles [2][64][P]
   const int s = blockIdx.z;
   const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
   if (j0 > i0) return;
@@ -136,27 +158,27 @@ __global__ __launch_bounds__(256) void prefill_scores_dmma_kernel(
   const int u = per_head ? s / G : s;
   const int nh = per_head ? 1 : G;
   const int h0 = per_head ? s : s * G;
-  const double* K = kc + (int64_t)u * nc * D;
-  for (int e = threadIdx.x; e < 64 * D; e += 256) {
-    const int r = e / D, d = e - r * D;
-    sk[r * P + d] = j0 + r < nc ? K[(int64_t)(j0 + r) * D + d] : 0.0;
-  }
+  load_tile_async<D, P>(sk, kc + (int64_t)u * nc * D, j0, nc);
+  load_tile_async<D, P>(sq0, qc + (int64_t)h0 * nc * D, i0, nc);
   double res[8][2];
   const int ar = warp * 8 + (lane >> 2), ak = lane & 3;  // A fragment: row, k
   for (int j = 0; j < nh; ++j) {
-    const double* Q = qc + (int64_t)(h0 + j) * nc * D;
-    __syncthreads();  // previous head's sq reads done
-    for (int e = threadIdx.x; e < 64 * D; e += 256) {
-      const int r = e / D, d = e - r * D;
-      sq[r * P + d] = i0 + r < nc ? Q[(int64_t)(i0 + r) * D + d] : 0.0;
+    // the next head's tile streams in while this one is multiplied
+    if (j + 1 < nh) {
+      load_tile_async<D, P>(sq0 + ((j + 1) & 1) * 64 * P, qc + (int64_t)(h0 + j + 1) * nc * D, i0,
+                            nc);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
+    const double* q = sq0 + (j & 1) * 64 * P;
     double acc[8][2];
 #pragma unroll
     for (int t = 0; t < 8; ++t) acc[t][0] = acc[t][1] = 0.0;
 #pragma unroll 4
     for (int k0 = 0; k0 < D; k0 += 4) {
-      const double a = sq[ar * P + k0 + ak];
+      const double a = q[ar * P + k0 + ak];
 #pragma unroll
       for (int t = 0; t < 8; ++t) dmma_8x8x4(acc[t], a, sk[(t * 8 + (lane >> 2)) * P + k0 + ak]);
     }
@@ -168,6 +190,7 @@ __global__ __launch_bounds__(256) void prefill_scores_dmma_kernel(
         else if (agg == DHSA_AGG_MAX) res[t][e] = fmax(res[t][e], acc[t][e]);
         else res[t][e] = res[t][e] + acc[t][e];
       }
+    __syncthreads();  // buffer j & 1 is refilled two heads later
   }
   const int ri = i0 + warp * 8 + (lane >> 2);
 #pragma unroll
@@ -1223,7 +1246,7 @@ extern "C" int dhsa_prefill_scores(const double* q_centroids, const double* k_ce
   bool dmma = D == 128;
   if (const char* e = getenv("DHSA_SCORES_DMMA")) dmma = dmma && atoi(e) != 0;
   if (dmma) {
-    constexpr int smem = 2 * 64 * (128 + 4) * 8;
+    constexpr int smem = 3 * 64 * (128 + 4) * 8;
     cudaError_t e = cudaFuncSetAttribute(prefill_scores_dmma_kernel<128>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) {
