@@ -13,9 +13,16 @@ inputs; the per-step working set (~1.07 GB) is far larger than L2.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3]
   python bench.py --impl reference ...   # the reference algorithm on host cores
 
-Multi-GPU (torchrun, one process per GPU): each rank owns its own 32
-sequences (units are independent; no collective on the data path), so the
-whole-job value is sum of tokens / max-over-ranks time ("scaling": "weak").
+Multi-GPU (torchrun, one process per GPU; ``--gpus N`` without WORLD_SIZE
+launches the N ranks itself): C3 shards the HEADS of the 32-sequence batch
+(configs[2]: "heads sharded across 1/2/4/8 B200"): rank r serves kv heads
+[r*8/N, (r+1)*8/N) and their 4 q heads each, so the whole job is the same
+32 tokens per step ("scaling": "strong", value = 32 tokens / max-over-ranks
+step time).  (sequence, kv head) units are independent: no collective on the
+data path.  ``--shard batch`` gives every rank its own full batch instead
+(weak scaling).  ``--rank-proxy N`` times rank 0's share of an N-GPU
+heads-sharded job on one GPU (every rank has the same shape and no
+communication, so that is the N-GPU step time).
 """
 
 from __future__ import annotations
@@ -60,7 +67,7 @@ def peaks():
 
 def workload_desc(name):
     B, Hq, Hkv, D, L, blk, K, dt = CONFIGS[name]
-    return (f"{name} decode: B={B} seqs/GPU, Hq={Hq}, Hkv={Hkv}, d={D}, context={L}, "
+    return (f"{name} decode: B={B} sequences, Hq={Hq}, Hkv={Hkv}, d={D}, context={L}, "
             f"block={blk}, top_k={K} (budget {K * blk + 1} tokens), {dt} KV, "
             f"group-shared max selection")
 
@@ -141,31 +148,97 @@ def _cpu_unit(args):
     return (time.perf_counter() - t0) / steps
 
 
-def cpu_baseline(name, units_sample=None, steps=2, workers=None):
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def reference_available():
+    """The unmodified reference package installed by tools/install_reference.sh."""
+    return os.path.isdir(os.path.join(REF_DIR, "dhsa"))
+
+
+def _ref_unit(args):
+    """One (sequence, kv-group) unit of the workload through the UNMODIFIED
+    reference package (baseline/_ref/dhsa): DecodeSession.__init__ builds the
+    centroid cache (aggregate_rows, chunk_repr.py:57-68; one-time, excluded),
+    then per step the reference's own decode-row composition (masks.py:153-173)
+    with the group-shared max of harness.aggregated_chunk_scores
+    (harness.py:288-306): scores of the G q-heads against [cached centroids |
+    gen_sum/sqrt(g) | aggregate_chunk(k)], max over heads, np.repeat over
+    extend_for_decode lengths, masks.topk_row; then the dense_attention row
+    body (core.py:115-118, softmax_row) for each of the G heads, and the
+    running-sum update of DecodeSession.step (masks.py:235-236).
+    Returns seconds per step."""
+    seed, L, D, G, block, budget, steps = args
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    from dhsa import DecodeSession, aggregate_chunk, extend_for_decode, softmax_row, \
+        static_boundaries, topk_row
+
+    rng = np.random.default_rng(seed)
+    k = rng.standard_normal((L + steps, D), dtype=np.float32).astype(np.float64)
+    v = rng.standard_normal((L + steps, D), dtype=np.float32).astype(np.float64)
+    q = rng.standard_normal((steps, G, D), dtype=np.float32).astype(np.float64)
+    sess = DecodeSession(k[:L], static_boundaries(L, block), budget)
+    inv = 1.0 / np.sqrt(D)
+    t0 = time.perf_counter()
+    for s in range(steps):
+        g = sess._gen_count
+        total = L + g + 1
+        parts = [sess.cached_chunk_keys]
+        if g >= 1:
+            parts.append((sess._gen_sum / np.sqrt(g))[None, :])
+        parts.append(aggregate_chunk(k[L + s][None, :])[None, :])
+        chunk_keys = np.concatenate(parts, axis=0)
+        scores = np.einsum("hd,jd->hj", q[s], chunk_keys).max(axis=0)
+        lens = np.diff(np.asarray(extend_for_decode(sess.prompt_bounds, total), dtype=np.intp))
+        idx = topk_row(np.repeat(scores, lens), total - 1, budget)
+        for j in range(G):
+            sc = np.einsum("jd,d->j", k[idx], q[s, j]) * inv
+            softmax_row(sc) @ v[idx]
+        sess._gen_sum += k[L + s]
+        sess._gen_count += 1
+    return (time.perf_counter() - t0) / steps
+
+
+def cpu_baseline(name, units_sample=None, steps=2, workers=None, shape=None):
+    """The reference decode step on the host cores, one single-threaded
+    process per core over independent (sequence, kv-group) units.  Uses the
+    unmodified reference package (kind "reference") when baseline/_ref holds
+    it, else the oracle port (kind "port").  ``shape`` overrides the
+    (B, Hq, Hkv) of the config (a rank's share of a heads-sharded job)."""
     import multiprocessing as mp
 
     B, Hq, Hkv, D, L, blk, K, _ = CONFIGS[name]
+    if shape is not None:
+        B, Hq, Hkv = shape
     G = Hq // Hkv
     workers = workers or min(32, os.cpu_count() or 1)  # ~0.4 GB of host RAM per unit
     units_total = B * Hkv
     n = units_sample or min(units_total, max(workers, 8))
     n = min(n, units_total)
+    use_ref = reference_available()
+    fn = _ref_unit if use_ref else _cpu_unit
     args = [(1000 + i, L, D, G, blk, K * blk + 1, steps) for i in range(n)]
     ctx = mp.get_context("fork")
     t0 = time.perf_counter()
     with ctx.Pool(min(workers, n)) as pool:
-        per_unit = pool.map(_cpu_unit, args)
+        per_unit = pool.map(fn, args)
     wall = time.perf_counter() - t0
     per_unit_s = float(np.mean(per_unit))
     used = min(workers, n)
     # whole-batch step time with `used` cores working on independent units
     step_s = per_unit_s * units_total / used
+    what = ("the unmodified reference package (baseline/_ref/dhsa: DecodeSession cache, "
+            "extend_for_decode + np.repeat + masks.topk_row select over the head-max scores, "
+            f"softmax_row attention rows for {G} heads)" if use_ref else
+            "oracle/dhsa_oracle.py reference formulation (repeat + stable argsort "
+            f"select, fp64 row attention for {G} heads)")
     return {
-        "value": B / step_s, "unit": "tokens/s", "cores": used, "kind": "port",
+        "value": B / step_s, "unit": "tokens/s", "cores": used,
+        "kind": "reference" if use_ref else "port",
         "us_per_step": step_s * 1e6,
         "sample": (f"{n} of {units_total} (sequence, kv-group) units x {steps} steps of {name}, "
-                   f"oracle/dhsa_oracle.py reference formulation (repeat + stable argsort "
-                   f"select, fp64 row attention for {G} heads), {used} processes; "
+                   f"{what}, {used} processes; "
                    f"{per_unit_s * 1e3:.1f} ms per unit-step, scaled to {units_total} units; "
                    f"wall {wall:.1f}s incl. setup"),
     }
@@ -222,6 +295,37 @@ def load_traffic():
     return {}
 
 
+def rank_shape(name, shard, parts):
+    """(B, Hq, Hkv) one rank runs: the config's shape ("batch": every rank
+    owns its own full batch, weak scaling) or 1/parts of the heads ("heads":
+    the config's batch with Hq/parts q heads and Hkv/parts kv heads per rank,
+    strong scaling; BASELINE.json configs[2] "heads sharded across 1/2/4/8")."""
+    B, Hq, Hkv = CONFIGS[name][:3]
+    if shard == "heads" and parts > 1:
+        if Hkv % parts:
+            raise SystemExit(f"{Hkv} kv heads cannot be sharded over {parts} ranks")
+        return B, Hq // parts, Hkv // parts
+    return B, Hq, Hkv
+
+
+def bench_config(name, world, shard, proxy, B, Hq, Hkv, dec=None):
+    """The config dict of both arms (ours and --impl reference)."""
+    _, Hq0, Hkv0, D, L, blk, K, dt = CONFIGS[name]
+    parts = proxy or world
+    cfg = {"workload": workload_desc(name), "context": L, "block": blk, "top_k": K,
+           "budget": K * blk + 1, "selection": "group-shared max over q-heads",
+           "sharding": (f"heads: {Hq}q/{Hkv}kv heads of {Hq0}/{Hkv0} per rank x {parts} ranks"
+                        if shard == "heads" and parts > 1 else
+                        f"batch: every rank owns {B} sequences"),
+           "global_batch": B if shard == "heads" else B * world,
+           "parallelism": (f"heads{parts}" if shard == "heads" and parts > 1 else f"dp{world}")}
+    if proxy:
+        cfg["rank_proxy"] = (f"one rank's share of a {proxy}-GPU heads-sharded job timed on this "
+                             f"GPU; ranks are independent (no collective on the data path), "
+                             f"so the {proxy}-GPU job time = this rank's time")
+    return cfg
+
+
 def run_gpu(args):
     import torch
 
@@ -229,7 +333,10 @@ def run_gpu(args):
 
     world, rank, local = dist_setup()
     name = args.config
-    B, Hq, Hkv, D, L, blk, K, dtn = CONFIGS[name]
+    _, _, _, D, L, blk, K, dtn = CONFIGS[name]
+    shard = args.shard or ("heads" if name == "C3" else "batch")
+    proxy = args.rank_proxy if world == 1 and args.rank_proxy and args.rank_proxy > 1 else 0
+    B, Hq, Hkv = rank_shape(name, shard, proxy or world)
     dtype = getattr(torch, dtn)
     W, S = args.warmup, args.steps
     roll = args.roll_steps  # untimed replays before/after the timed steps (clock sampling)
@@ -286,7 +393,9 @@ def run_gpu(args):
     ms = max_over_ranks(ms, world)
     ms_step = ms / S
     dec.steps += W + S + 2 * roll
-    value = B * world * S / (ms / 1e3)
+    # whole-job tokens/s: heads-sharded ranks all serve the same B sequences
+    seqs = B if shard == "heads" else B * world
+    value = seqs * S / (ms / 1e3)
 
     # per-kernel breakdown (eager launches bracketed by events, same stream)
     names = None
@@ -336,28 +445,46 @@ def run_gpu(args):
             dec.step_host_packed(hqkv, hout)
         e1.record(stream)
         torch.cuda.synchronize()
+    e2e_pipe_ms = max_over_ranks(e0.elapsed_time(e1) / ne, world)
+    # a real decode loop: step i+1's q exists only after step i's output is
+    # on the host, so every step waits for its own D2H copy before the next
+    # H2D copy is issued (host synchronisation inside the timed region)
+    torch.cuda.synchronize()
+    barrier(world)
+    with torch.cuda.stream(stream):
+        dec.step_host_packed(hqkv, hout)
+        stream.synchronize()
+        e0.record(stream)
+        for i in range(ne):
+            dec.step_host_packed(hqkv, hout)
+            stream.synchronize()
+        e1.record(stream)
+        torch.cuda.synchronize()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / ne, world)
     esz = torch.finfo(dtype).bits // 8
     h2d = (B * Hq * D + 2 * B * Hkv * D) * esz
     d2h = B * Hq * D * esz
 
     step_mb = (bytes_["centroids"] + bytes_["kv"]) / 1e6
+    cfg = bench_config(name, world, shard, proxy, B, Hq, Hkv)
+    cfg.update({
+        "rank_shape": {"batch": B, "q_heads": Hq, "kv_heads": Hkv},
+        "l2": (f"per-rank working set larger than L2 (126 MB): sketch "
+               f"{bytes_['centroids'] / 1e6:.0f} MB + selected KV {bytes_['kv'] / 1e6:.0f} MB per "
+               f"step, read once; a step's 32 distinct q/k/v inputs rotate"
+               if step_mb > 126 else
+               f"per-rank working set ({step_mb:.0f} MB/step) of the same order as L2 and not "
+               f"flushed; the KV cache behind it ({dec.k_cache.numel() * 4 / 1e9:.1f} GB) is not"),
+        "graphs": f"one CUDA graph per step ({dec.kernels_per_step} kernels)",
+        "scoring": dec.scoring, "attention": dec.attn_mode})
     result = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": S,
         "warmup": W, "ms_per_step": ms_step, "us_per_step": ms_step * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong" if shard == "heads" else "weak",
+        "vs_baseline": None,
         "dtype": "bf16" if dtype == torch.bfloat16 else "f32",
         "data": f"synthetic N(0,1) q/k/v, random-init KV cache; {step_mb:.0f} MB read per step",
-        "config": {"workload": workload_desc(name), "batch_per_gpu": B, "global_batch": B * world,
-                   "context": L, "block": blk, "top_k": K, "budget": K * blk + 1,
-                   "selection": "group-shared max over q-heads", "parallelism": f"dp{world}",
-                   "l2": (f"inputs larger than L2 (126 MB): sketch {bytes_['centroids'] / 1e6:.0f} MB"
-                          f" + selected KV {bytes_['kv'] / 1e6:.0f} MB per step"
-                          if step_mb > 126 else
-                          f"inputs ({step_mb:.0f} MB/step) fit in L2 and are not flushed: a "
-                          "latency-bound demo shape, not an HBM roofline case"),
-                   "graphs": f"one CUDA graph per step ({dec.kernels_per_step} kernels)",
-                   "scoring": dec.scoring, "attention": dec.attn_mode},
+        "config": cfg,
         "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "algorithmic_bytes": kern_bytes[dominant]},
@@ -365,18 +492,24 @@ def run_gpu(args):
                           "achieved_gbs": bytes_["total"] / (ms_step * 1e-3) / 1e9,
                           "frac": bytes_["total"] / (ms_step * 1e-3) / 1e9 / peak},
         "breakdown_us": us,
-        "e2e": {"value": B * world / (e2e_ms / 1e3), "unit": "tokens/s",
+        "e2e": {"value": seqs / (e2e_ms / 1e3), "unit": "tokens/s",
                 "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "path": "SparseDecoder.step_host_packed (public API: one pinned host [q|k|v] "
                         "buffer -> one H2D copy -> one CUDA-graph replay of the C-ABI kernels -> "
-                        "host o)"},
+                        "host o), the host waiting for each step's output before issuing the "
+                        "next (an autoregressive decode loop)",
+                "pipelined": {"value": seqs / (e2e_pipe_ms / 1e3), "ms_per_step": e2e_pipe_ms,
+                              "note": "steps enqueued back to back without host waits (copy of "
+                                      "step i overlaps step i+1): throughput, not latency"}},
         "gpu_launches": dec.kernels_per_step * S,
         "clocks": clk.summary(),
         "splits": dec.splits if dec.attn_mode == "split" else None,
     }
+    if proxy:
+        result["proxy"] = {"n_gpus": proxy, "note": cfg["rank_proxy"]}
     if rank == 0 and world == 1 and not args.no_cpu:
-        # ~10-20 s of host CPU work: 16+ units x 8 decode steps
-        result["cpu_baseline"] = cpu_baseline(name, units_sample=args.cpu_units or 64, steps=8)
+        # ~10-30 s of host CPU work: 64 units x 4 decode steps of the whole job
+        result["cpu_baseline"] = cpu_baseline(name, units_sample=args.cpu_units or 64, steps=4)
     if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:
@@ -642,32 +775,54 @@ def run_gpu_c5(args):
 
 
 def run_reference(args):
+    """The reference arm: the reference's own CPU implementation of the path
+    (baseline/_ref, else the oracle port) on this box's host cores, on the
+    same workload, metric and config as our arm; rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
     name = args.config if args.config in CONFIGS else "C3"
-    B = CONFIGS[name][0]
+    shard = args.shard or ("heads" if name == "C3" else "batch")
+    proxy = args.rank_proxy if world == 1 and args.rank_proxy and args.rank_proxy > 1 else 0
+    B, Hq, Hkv = rank_shape(name, shard, proxy or world)
+    seqs = B if shard == "heads" else B * world
     vals = []
     cb = None
-    # each step: one bounded sample (16 units x 1 decode step) of the workload
+    # each step: one bounded sample (units x 1 decode step) of the whole job
+    # (its units are independent; the host cores serve all of them)
     for i in range(args.warmup_ref + args.steps_ref):
         cb = cpu_baseline(name, units_sample=args.cpu_units, steps=1)
         if i >= args.warmup_ref:
             vals.append(cb["value"])
-    value = float(np.mean(vals))
+    value = float(np.mean(vals)) * seqs / CONFIGS[name][0]
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
         "n_gpus": world, "steps": args.steps_ref, "warmup": args.warmup_ref,
-        "ms_per_step": B / value * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": seqs / value * 1e3, "higher_is_better": True,
+        "scaling": "strong" if shard == "heads" else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic N(0,1), fp32-valued",
-        "config": {"workload": workload_desc(name), "batch_per_gpu": B, "context": CONFIGS[name][4]},
+        "config": bench_config(name, world, shard, proxy, B, Hq, Hkv),
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cb["cores"],
-                         "kind": "port", "sample": cb["sample"]},
+                         "kind": cb["kind"], "sample": cb["sample"]},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def self_launch(args):
+    """``--gpus N`` (N > 1) outside torchrun: run N ranks of this script
+    under torch.distributed.run on 127.0.0.1 and return its exit code."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -688,7 +843,14 @@ def main():
     ap.add_argument("--no-quality", action="store_true")
     ap.add_argument("--no-dynamic", action="store_true",
                     help="C5: skip the predictor -> NMS -> dynamic-chunk prefill run")
+    ap.add_argument("--shard", default=None, choices=[None, "heads", "batch"],
+                    help="multi-GPU decode: shard the heads of one batch (C3 default) or give "
+                         "every rank its own batch")
+    ap.add_argument("--rank-proxy", type=int, default=0,
+                    help="one GPU: time rank 0's share of an N-GPU heads-sharded job")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     args.warmup = max(args.warmup, 3)
     # the reference arm: every "step" is one bounded CPU sample (~0.6 s)
     args.steps_ref = max(1, args.steps)

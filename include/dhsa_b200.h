@@ -104,7 +104,15 @@ int dhsa_decode_score(int dtype, const void* q, const double* centroids,
 int dhsa_decode_select(const double* scores, int64_t sc_stride, dhsa_layout layout,
                        const int32_t* gen_count, int U, int heads_per_unit,
                        int64_t budget, int tile_tokens, int32_t* tiles,
-                       int64_t tile_cap, int32_t* ntiles, dhsa_stream_t stream);
+                       int64_t tile_cap, int32_t* ntiles, void* scratch,
+                       dhsa_stream_t stream);
+
+/* Bytes of global scratch PER SELECTION ROW that dhsa_decode_select /
+ * dhsa_rows_select need for rows of `n_chunks` chunks (decode: max_chunks+1).
+ * 0 = the row's keys fit in shared memory and `scratch` may be NULL;
+ * otherwise `scratch` must hold rows * this many bytes (topk_row over more
+ * than ~17K token positions, where every position is its own chunk). */
+int64_t dhsa_select_scratch_size(int n_chunks);
 
 /* K5/K6 — exact attention over selected token tiles: per q-head,
  * softmax(K[idx] q / sqrt(D)) @ V[idx] (core.py:113-118) with an online
@@ -171,7 +179,8 @@ int dhsa_chunk_scores(const double* qc, const double* kc, int n, int m, int D,
 int dhsa_rows_select(const double* scores, int64_t sc_stride, const int32_t* bounds,
                      int n_chunks, const int32_t* row_index, int rows,
                      int64_t budget, int tile_tokens, int32_t* tiles,
-                     int64_t tile_cap, int32_t* ntiles, dhsa_stream_t stream);
+                     int64_t tile_cap, int32_t* ntiles, void* scratch,
+                     dhsa_stream_t stream);
 
 /* ---- bf16 fast path: fp16 centroid sketch + certified exact selection -----
  * The decode step for bf16 caches streams an fp16 copy ("sketch") of the fp64

@@ -75,3 +75,13 @@ def tile_capacity(n_chunks: int, budget: int, length: int, tile: int) -> int:
     ceil(take/tile) tiles, sum(take) <= budget-1, plus the self tile."""
     r = max(0, min(int(budget), int(length)) - 1)
     return int(min(n_chunks, r) + r // tile + 2)
+
+
+def select_scratch(n_chunks: int, rows: int):
+    """Global scratch for dhsa_decode_select / dhsa_rows_select when a row's
+    chunk keys exceed shared memory (None when they fit)."""
+    import torch
+
+    per = int(_lib.load().dhsa_select_scratch_size(int(n_chunks)))
+    return None if per == 0 else torch.empty(per * max(1, int(rows)), dtype=torch.uint8,
+                                              device=device())

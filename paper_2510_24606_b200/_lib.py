@@ -62,7 +62,8 @@ _SIGS = {
     "dhsa_decode_score": (C.c_int, [C.c_int, vp, vp, C.c_int64, vp, vp, vp, vp, vp, vp, C.c_int64,
                                     Layout, C.c_int, C.c_int, C.c_int, C.c_int, vp, C.c_int64, vp]),
     "dhsa_decode_select": (C.c_int, [vp, C.c_int64, Layout, vp, C.c_int, C.c_int, C.c_int64,
-                                     C.c_int, vp, C.c_int64, vp, vp]),
+                                     C.c_int, vp, C.c_int64, vp, vp, vp]),
+    "dhsa_select_scratch_size": (C.c_int64, [C.c_int]),
     "dhsa_attn_workspace_size": (C.c_int64, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]),
     "dhsa_attn": (C.c_int, [C.c_int, vp, vp, vp, C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int,
                             C.c_int, vp, C.c_int64, vp, C.c_int, vp, vp, vp, vp, vp]),
@@ -70,7 +71,7 @@ _SIGS = {
     "dhsa_chunk_scores": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64,
                                     C.c_int64, vp, C.c_int64, vp]),
     "dhsa_rows_select": (C.c_int, [vp, C.c_int64, vp, C.c_int, vp, C.c_int, C.c_int64, C.c_int,
-                                   vp, C.c_int64, vp, vp]),
+                                   vp, C.c_int64, vp, vp, vp]),
     "dhsa_upsample": (C.c_int, [vp, vp, C.c_int, C.c_int, vp, vp]),
     "dhsa_sketch_build": (C.c_int, [vp, C.c_int64, C.c_int, C.c_int, Layout, vp, C.c_int64, vp,
                                     vp]),

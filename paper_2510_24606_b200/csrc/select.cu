@@ -20,6 +20,11 @@
 #include "capi.cuh"
 #include "walk.cuh"
 
+extern "C" int64_t dhsa_select_scratch_size(int n_chunks) {
+  const int64_t bytes = ((int64_t)n_chunks * (sizeof(uint64_t) + sizeof(int32_t)) + 15) / 16 * 16;
+  return bytes <= 200 * 1024 ? 0 : bytes;
+}
+
 namespace dhsa {
 
 constexpr int kSelThreads = 512;
@@ -92,14 +97,19 @@ __global__ __launch_bounds__(kSelThreads) void select_kernel(View view, int64_t 
                                                              int tile_tokens,
                                                              int32_t* __restrict__ tiles,
                                                              int64_t tile_cap,
-                                                             int32_t* __restrict__ ntiles) {
+                                                             int32_t* __restrict__ ntiles,
+                                                             unsigned char* gscratch,
+                                                             int64_t gscratch_stride) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ WalkShared sh;
   const int item = blockIdx.x;
   view.init(item);
   const int n = view.n();
   const int row = view.row();
-  uint64_t* keys = reinterpret_cast<uint64_t*>(smem_raw);
+  // keys + lengths in shared memory, or (rows of more chunks than fit, e.g.
+  // topk_row with one chunk per token beyond ~17K positions) in global scratch
+  unsigned char* base = gscratch ? gscratch + (int64_t)item * gscratch_stride : smem_raw;
+  uint64_t* keys = reinterpret_cast<uint64_t*>(base);
   int32_t* lens = reinterpret_cast<int32_t*>(keys + n);
   for (int c = threadIdx.x; c < n; c += kSelThreads) {
     int lo, len;
@@ -123,11 +133,17 @@ __global__ __launch_bounds__(kSelThreads) void select_kernel(View view, int64_t 
 
 template <class View>
 static int launch_select(View v, int items, int n_max, int64_t budget, int tile_tokens,
-                         int32_t* tiles, int64_t tile_cap, int32_t* ntiles, cudaStream_t s,
-                         const char* name) {
-  const size_t smem = (size_t)n_max * (sizeof(uint64_t) + sizeof(int32_t));
-  DHSA_REQUIRE(smem <= 200 * 1024, "%s: %d chunks exceed the shared-memory select capacity",
-               name, n_max);
+                         int32_t* tiles, int64_t tile_cap, int32_t* ntiles, void* scratch,
+                         cudaStream_t s, const char* name) {
+  const int64_t need = dhsa_select_scratch_size(n_max);
+  size_t smem = 0;
+  if (need == 0) {
+    smem = (size_t)n_max * (sizeof(uint64_t) + sizeof(int32_t));
+    scratch = nullptr;
+  } else {
+    DHSA_REQUIRE(scratch, "%s: %d chunks need %lld bytes of global select scratch per row",
+                 name, n_max, (long long)need);
+  }
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(select_kernel<View>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -137,7 +153,7 @@ static int launch_select(View v, int items, int n_max, int64_t budget, int tile_
     }
   }
   select_kernel<View><<<items, kSelThreads, smem, s>>>(v, budget, tile_tokens, tiles, tile_cap,
-                                                       ntiles);
+                                                       ntiles, (unsigned char*)scratch, need);
   return check_launch(name);
 }
 
@@ -148,7 +164,8 @@ using namespace dhsa;
 extern "C" int dhsa_decode_select(const double* scores, int64_t sc_stride, dhsa_layout layout,
                                   const int32_t* gen_count, int U, int heads_per_unit,
                                   int64_t budget, int tile_tokens, int32_t* tiles,
-                                  int64_t tile_cap, int32_t* ntiles, dhsa_stream_t stream) {
+                                  int64_t tile_cap, int32_t* ntiles, void* scratch,
+                                  dhsa_stream_t stream) {
   DHSA_REQUIRE(scores && gen_count && tiles && ntiles, "dhsa_decode_select: null pointer");
   DHSA_REQUIRE(budget >= 1, "budget must be >= 1");
   DHSA_REQUIRE(U >= 1 && heads_per_unit >= 1 && tile_tokens >= 1 && tile_cap >= 1,
@@ -156,18 +173,19 @@ extern "C" int dhsa_decode_select(const double* scores, int64_t sc_stride, dhsa_
   DHSA_REQUIRE(valid_layout(layout), "dhsa_decode_select: bad layout");
   DecodeRows v{scores, sc_stride, Layout(layout), gen_count, heads_per_unit};
   return launch_select(v, U * heads_per_unit, layout.max_chunks + 1, budget, tile_tokens, tiles,
-                       tile_cap, ntiles, (cudaStream_t)stream, "dhsa_decode_select");
+                       tile_cap, ntiles, scratch, (cudaStream_t)stream, "dhsa_decode_select");
 }
 
 extern "C" int dhsa_rows_select(const double* scores, int64_t sc_stride, const int32_t* bounds,
                                 int n_chunks, const int32_t* row_index, int rows,
                                 int64_t budget, int tile_tokens, int32_t* tiles,
-                                int64_t tile_cap, int32_t* ntiles, dhsa_stream_t stream) {
+                                int64_t tile_cap, int32_t* ntiles, void* scratch,
+                                dhsa_stream_t stream) {
   DHSA_REQUIRE(scores && bounds && row_index && tiles && ntiles, "dhsa_rows_select: null pointer");
   DHSA_REQUIRE(budget >= 1, "budget must be >= 1");
   DHSA_REQUIRE(n_chunks >= 1 && rows >= 1 && tile_tokens >= 1 && tile_cap >= 1,
                "dhsa_rows_select: bad shape");
   MatrixRows v{scores, sc_stride, bounds, n_chunks, row_index};
-  return launch_select(v, rows, n_chunks, budget, tile_tokens, tiles, tile_cap, ntiles,
+  return launch_select(v, rows, n_chunks, budget, tile_tokens, tiles, tile_cap, ntiles, scratch,
                        (cudaStream_t)stream, "dhsa_rows_select");
 }

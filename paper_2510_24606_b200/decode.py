@@ -130,6 +130,10 @@ class SparseDecoder:
             per_unit = _lib.load().dhsa_sketch_select_scratch_size(self.nc_cap)
             self.scratch = (torch.empty(self.U * per_unit, dtype=torch.uint8, **kw)
                             if per_unit > 0 else None)
+        # fp64 scoring: the select kernel's global scratch for very long units
+        per_row = _lib.load().dhsa_select_scratch_size(self.nc_cap + 1)
+        self.sel_scratch = (torch.empty(per_row * self.items, dtype=torch.uint8, **kw)
+                            if per_row > 0 and self.scoring == "fp64" else None)
 
     # ------------------------------------------------------------------
     def _layout(self):
@@ -170,6 +174,12 @@ class SparseDecoder:
         P = keys.shape[2] if prompt_len is None else int(prompt_len)
         if P < 1 or P + 1 > self.L_cap - 64:
             raise ValueError("prompt does not fit the cache")
+        if bounds is None and (P + self.block - 1) // self.block > self.nc_cap:
+            raise ValueError(f"a {P}-token prompt has {(P + self.block - 1) // self.block} "
+                             f"chunks of {self.block}; the decoder holds {self.nc_cap}")
+        # the captured step graphs bake in the chunk layout (max_chunks, the
+        # bounds / nchunks pointers): a new prompt needs new captures
+        self._graph = self._pgraph = None
         self._set_bounds(bounds, P)
         self.k_cache[:, :, :P].copy_(keys[:, :, :P])
         self.v_cache[:, :, :P].copy_(values[:, :, :P])
@@ -299,7 +309,7 @@ class SparseDecoder:
             _lib.call("dhsa_decode_select", _lib.ptr(self.scores), self.nc_cap + 1, lay,
                       _lib.ptr(self.gen_count), self.U, self.G if self.per_head else 1,
                       self.budget, self.tile, _lib.ptr(self.tiles), self.tile_cap,
-                      _lib.ptr(self.ntiles), st)
+                      _lib.ptr(self.ntiles), _lib.ptr(self.sel_scratch), st)
 
         def advance():
             _lib.call("dhsa_decode_advance", _lib.ptr(self.gen_count), self.U, st)

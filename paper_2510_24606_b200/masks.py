@@ -103,9 +103,10 @@ def _rows_select(scores_dev_t, sc_stride, bounds, rows, budget):
     # device temporaries must outlive the (asynchronous) launch: the caching
     # allocator would otherwise hand their memory to the next allocation
     b_dev, r_dev = _dev.i32(bounds), _dev.i32(rows)
+    scratch = _dev.select_scratch(n, len(rows))
     _lib.call("dhsa_rows_select", _lib.ptr(scores_dev_t), int(sc_stride), _lib.ptr(b_dev), n,
               _lib.ptr(r_dev), len(rows), int(budget), TILE, _lib.ptr(tiles), cap,
-              _lib.ptr(ntiles), _dev.stream())
+              _lib.ptr(ntiles), _lib.ptr(scratch), _dev.stream())
     return _dev.tiles_to_rows(_dev.host(tiles), _dev.host(ntiles))
 
 
@@ -189,9 +190,10 @@ class _DecodeState:
         cap = _dev.tile_capacity(self.n + 1, budget, length, TILE)
         tiles = _dev.empty((1, cap, 2), dtype=torch.int32)
         ntiles = _dev.empty((1,), dtype=torch.int32)
+        scratch = _dev.select_scratch(self.n + 1, 1)
         _lib.call("dhsa_decode_select", _lib.ptr(self.scores), self.n + 1, lay,
                   _lib.ptr(self.gen_count), 1, 1, int(budget), TILE, _lib.ptr(tiles), cap,
-                  _lib.ptr(ntiles), st)
+                  _lib.ptr(ntiles), _lib.ptr(scratch), st)
         if update:
             _lib.call("dhsa_decode_advance", _lib.ptr(self.gen_count), 1, st)
         return _dev.tiles_to_rows(_dev.host(tiles), _dev.host(ntiles))[0]

@@ -74,6 +74,9 @@ class SparsePrefill:
         self.plen_q = torch.full((self.U * self.G,), seq_len, dtype=torch.int32, device=dev)
         self.plen_k = torch.full((self.U,), seq_len, dtype=torch.int32, device=dev)
         self.counters = torch.zeros(2, dtype=torch.int32, device=dev)  # persistent attention
+        # __call__ verifies the plan capacity (one device sync); benchmarks that
+        # time back-to-back calls switch it off and call check_capacity() once
+        self.checked = True
         self.nc = self.cap = 0
         self.set_bounds(bounds)
 
@@ -116,7 +119,9 @@ class SparsePrefill:
             walk_blocks = (self.budget - 1 + _TOK - 1) // _TOK + most
             need = np.minimum(pref[:-1], walk_blocks) + nblk
             cap = max(cap, int(need.max()))
-        cap = min(cap, _PLAN_CAP)
+        if cap > _PLAN_CAP:
+            raise ValueError(f"budget {self.budget} over these chunks needs up to {cap} plan "
+                             f"entries per query chunk (limit {_PLAN_CAP})")
         kb = np.full((len(lists), nc + 1), L, dtype=np.int32)
         for u, b in enumerate(lists):
             kb[u, :len(b)] = b
@@ -215,6 +220,10 @@ class SparsePrefill:
             out = torch.empty_like(q)
         for _, fn in self.stages(q, k, v, out, stream, row_stats):
             fn()
+        if self.checked:
+            # a plan that overflowed its capacity leaves its query tile
+            # unwritten: fail loudly instead of returning garbage rows
+            self.check_capacity()
         return out
 
     def mask_bitsets(self, stream=None):

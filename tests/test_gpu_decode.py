@@ -337,3 +337,58 @@ def test_tiny_prompts(P):
                top_k=1, dtype=torch.bfloat16, agg="max")
     worst = run_and_check(dec, t, host, P, steps, "max")
     assert worst <= TOL[torch.bfloat16], worst
+
+
+def test_step_host_after_second_prefill():
+    """A decoder that already captured its step graph is prefilled again with
+    a LONGER prompt and then with explicit (dynamic) bounds: the serving
+    entry points re-capture and match eager steps bit for bit (the captured
+    graph bakes in max_chunks and the bounds pointers)."""
+    B, Hq, Hkv, D, steps = 2, 8, 2, 128, 3
+    P1, P2 = 700, 1900
+    t, _ = make_inputs(B, Hq, Hkv, D, P2, steps, torch.bfloat16, seed=44)
+    rng = np.random.default_rng(5)
+    dyn = _random_bounds(rng, P2, lo=8, hi=120)
+
+    def run(mode, prompts):
+        dec = _dec(batch=B, q_heads=Hq, kv_heads=Hkv, head_dim=D, max_len=P2 + steps,
+                   block=64, top_k=5, dtype=torch.bfloat16, agg="max",
+                   max_chunks=max(len(dyn), 64))
+        outs = []
+        for P, bounds in prompts:
+            dec.prefill(t["k"][:, :, :P].cuda(), t["v"][:, :, :P].cuda(), bounds=bounds)
+            for s in range(steps):
+                q, k, v = (t[n][:, :, s if n == "q" else P + s].contiguous()
+                           for n in ("q", "k", "v"))
+                if mode == "eager":
+                    o = dec.step(q.cuda(), k.cuda(), v.cuda()).cpu()
+                elif mode == "host":
+                    o = torch.empty(B, Hq, D, dtype=torch.bfloat16).pin_memory()
+                    dec.step_host(q.pin_memory(), k.pin_memory(), v.pin_memory(), o)
+                    torch.cuda.synchronize()
+                else:
+                    qkv = torch.cat([q.reshape(-1), k.reshape(-1), v.reshape(-1)]).pin_memory()
+                    o = torch.empty(B, Hq, D, dtype=torch.bfloat16).pin_memory()
+                    dec.step_host_packed(qkv, o)
+                    torch.cuda.synchronize()
+                outs.append((o.clone(), [x.copy() for x in dec.selection()]))
+        return outs
+
+    prompts = [(P1, None), (P2, None), (P2, dyn)]
+    ref = run("eager", prompts)
+    for mode in ("host", "packed"):
+        got = run(mode, prompts)
+        for (oa, sa), (ob, sb) in zip(ref, got):
+            assert torch.equal(oa, ob), mode
+            for a, b in zip(sa, sb):
+                assert np.array_equal(a, b), mode
+
+
+def test_static_prompt_longer_than_chunk_capacity():
+    """A static-grid prompt whose chunk count exceeds the decoder's chunk
+    capacity is refused (it would overwrite the next unit's centroids)."""
+    dec = _dec(batch=1, q_heads=4, kv_heads=1, head_dim=128, max_len=100, block=16, top_k=2,
+               dtype=torch.bfloat16, agg="max")
+    k = torch.zeros(1, 1, 127, 128, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(ValueError, match="chunks"):
+        dec.prefill(k, k, prompt_len=127)

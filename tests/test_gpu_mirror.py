@@ -152,3 +152,15 @@ def test_dense_attention_masked_vs_oracle(rng):
         rows = [sorted(set(j for j in range(i) if rng.random() < 0.5) | {i}) for i in range(L)]
         want = O.attend_rows(seq.queries, seq.keys, seq.values, rows)
         np.testing.assert_allclose(P.dense_attention(seq, rows), want, atol=1e-12)
+
+
+def test_topk_row_beyond_shared_memory(rng):
+    """topk_row over ~40K positions (one chunk per token, more keys than the
+    select's shared memory holds): the global-scratch select gives the
+    reference's row (masks.py:103-122), ties included."""
+    s = rng.standard_normal(40000)
+    s[100:300] = s[5]  # a tie class
+    for row, budget in ((39999, 4097), (30000, 20000), (39999, 1), (25000, 40000)):
+        want = O.token_topk(s, row, budget)
+        assert np.array_equal(P.topk_row(s, row, budget), want), (row, budget)
+

@@ -325,3 +325,15 @@ def test_predictor_nms_prefill_pipeline():
     worst = _run(B=1, Hq=8, Hkv=Hkv, L=L, budget=300, agg="max", seed=23, bounds=bounds,
                  check_rows=range(0, L, 3))
     assert worst <= TOL_BF16, worst
+
+
+def test_prefill_plan_capacity_refused():
+    """Dynamic chunks so short that a walk of budget-1 tokens needs more plan
+    entries than a CTA stages: refused with ValueError (no silently
+    unwritten rows)."""
+    from paper_2510_24606_b200.prefill import SparsePrefill
+
+    L = 8192
+    bounds = list(range(0, L, 2)) + [L]
+    with pytest.raises(ValueError, match="plan"):
+        SparsePrefill(1, 4, 1, 128, L, budget=4097, agg="max", bounds=bounds)

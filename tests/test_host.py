@@ -147,11 +147,12 @@ def test_workspace_size_formula():
 
 def test_error_channel_without_device():
     lib = _lib.load()
-    rc = lib.dhsa_decode_select(None, 0, _lib.Layout(), None, 1, 1, 5, 64, None, 1, None, None)
+    rc = lib.dhsa_decode_select(None, 0, _lib.Layout(), None, 1, 1, 5, 64, None, 1, None, None,
+                                None)
     assert rc == -1
     assert b"null pointer" in lib.dhsa_last_error()
     rc = lib.dhsa_decode_select(ctypes.c_void_p(8), 0, _lib.Layout(), ctypes.c_void_p(8), 1, 1, 0,
-                                64, ctypes.c_void_p(8), 1, ctypes.c_void_p(8), None)
+                                64, ctypes.c_void_p(8), 1, ctypes.c_void_p(8), None, None)
     assert rc == -1
     assert b"budget must be >= 1" in lib.dhsa_last_error()
 

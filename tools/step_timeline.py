@@ -1,7 +1,8 @@
 """Timeline of one C3 decode step replayed from a CUDA graph: per-CTA
 %globaltimer stamps of the sketch stream, select and attention kernels
 (DHSA_DEBUG_TIMING, see common.cuh), printed relative to the earliest sketch
-CTA start.  Usage: python tools/step_timeline.py [B] [context]."""
+CTA start.  Usage: python tools/step_timeline.py [B] [context] [split]
+(TL_HQ / TL_HKV set the heads)."""
 import os
 import sys
 
@@ -13,7 +14,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 32
 L = int(sys.argv[2]) if len(sys.argv) > 2 else 131072
 SPLIT = len(sys.argv) > 3 and sys.argv[3] == "split"  # C4 path: one shard, LocalComm
-Hq, Hkv, D = 32, 8, 128
+# heads per rank (the C3 heads-sharded rank proxy: 32/N q heads, 8/N kv heads)
+Hq = int(os.environ.get("TL_HQ", 32))
+Hkv = int(os.environ.get("TL_HKV", 8))
+D = 128
 dbg = torch.zeros(262144, dtype=torch.int64, device="cuda")
 os.environ["DHSA_DEBUG_TIMING"] = str(dbg.data_ptr())
 from paper_2510_24606_b200.decode import SparseDecoder  # noqa: E402
@@ -47,7 +51,8 @@ with torch.cuda.graph(gr, stream=s):
         shard.launch(q, k, v, comm, out, stream=s)
     else:
         dec.launch(q, k, v, out, stream=s)
-for _ in range(5):
+# keep the GPU busy long enough for the SM clock to reach its loaded value
+for _ in range(int(os.environ.get("TL_WARM", 3000))):
     gr.replay()
 torch.cuda.synchronize()
 dbg.zero_()
