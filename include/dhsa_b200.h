@@ -403,6 +403,11 @@ int dhsa_predictor_forward(const double* keys, int L, int d, int window, int hea
                            const double* b1, const double* w2, double b2, void* workspace,
                            double* probs, dhsa_stream_t stream);
 
+/* softmax_row (core.py:69-77) of `rows` fp64 rows of n scores each:
+ * out = exp(s - max s) / sum(exp(s - max s)), per row. */
+int dhsa_softmax_rows(const double* scores, int rows, int64_t n, double* out,
+                      dhsa_stream_t stream);
+
 /* f_upsample (masks.upsample, masks.py:87-100): out[i][j] = s[chunk(i)][chunk(j)]
  * for an n x n chunk-score matrix and bounds [n+1]; out is L x L fp64.  Only
  * the drop-in API uses it — the selection kernels never materialise it. */

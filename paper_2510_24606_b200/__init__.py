@@ -10,7 +10,7 @@ device is missing.
 """
 
 from .chunking import check_boundaries, extend_for_decode, nms_boundaries, static_boundaries
-from .core import TokenSequence, dense_attention
+from .core import TokenSequence, dense_attention, softmax_row
 from .chunk_repr import ChunkReps, aggregate_chunk, aggregate_rows, build_chunk_reps, \
     chunk_similarity
 from . import predictor, serialization
@@ -20,7 +20,7 @@ from .masks import CostCounters, DecodeSession, SparsityMask, decode_mask_row, \
 __version__ = "0.1.0"
 
 __all__ = [
-    "TokenSequence", "dense_attention",
+    "TokenSequence", "softmax_row", "dense_attention",
     "check_boundaries", "static_boundaries", "nms_boundaries", "extend_for_decode",
     "ChunkReps", "aggregate_chunk", "aggregate_rows", "build_chunk_reps", "chunk_similarity",
     "CostCounters", "SparsityMask", "upsample", "topk_row", "mask_from_chunk_scores",

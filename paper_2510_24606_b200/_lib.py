@@ -73,6 +73,7 @@ _SIGS = {
     "dhsa_rows_select": (C.c_int, [vp, C.c_int64, vp, C.c_int, vp, C.c_int, C.c_int64, C.c_int,
                                    vp, C.c_int64, vp, vp, vp]),
     "dhsa_upsample": (C.c_int, [vp, vp, C.c_int, C.c_int, vp, vp]),
+    "dhsa_softmax_rows": (C.c_int, [vp, C.c_int, C.c_int64, vp, vp]),
     "dhsa_sketch_build": (C.c_int, [vp, C.c_int64, C.c_int, C.c_int, Layout, vp, C.c_int64, vp,
                                     vp]),
     "dhsa_sketch_select_scratch_size": (C.c_int64, [C.c_int]),

@@ -1,8 +1,8 @@
 """Drop-in for ``dhsa.core`` on the hot path: ``TokenSequence`` and the exact
 (masked) causal attention ``dense_attention``.
 
-Reference: core.py:35-66 (TokenSequence), core.py:80-119 (_mask_rows,
-dense_attention).  The attention runs on the GPU through ``dhsa_attn`` in
+Reference: core.py:35-66 (TokenSequence), core.py:69-77 (softmax_row),
+core.py:80-119 (_mask_rows, dense_attention).  The attention runs on the GPU through ``dhsa_attn`` in
 fp64 (DFMA, online softmax), so outputs agree with the float64 reference to
 ~1e-15; masks are validated on the host with the reference's error messages.
 """
@@ -15,7 +15,7 @@ import numpy as np
 
 from . import _dev, _lib
 
-__all__ = ["TokenSequence", "dense_attention"]
+__all__ = ["TokenSequence", "softmax_row", "dense_attention"]
 
 
 def _matrix(x, name):
@@ -55,6 +55,20 @@ class TokenSequence:
     @property
     def dim(self) -> int:
         return self.queries.shape[1]
+
+
+def softmax_row(scores) -> np.ndarray:
+    """Numerically stable softmax of a 1-D score vector (core.py:69-77),
+    computed in fp64 on the device (dhsa_softmax_rows)."""
+    s = np.asarray(scores, dtype=np.float64)
+    if s.ndim != 1 or s.size == 0:
+        raise ValueError("softmax_row expects a non-empty 1-D array")
+    if not np.all(np.isfinite(s)):
+        raise ValueError("softmax_row: non-finite scores")
+    x = _dev.f64(s)
+    out = _dev.empty((s.size,))
+    _lib.call("dhsa_softmax_rows", _lib.ptr(x), 1, s.size, _lib.ptr(out), _dev.stream())
+    return _dev.host(out)
 
 
 def _validated_rows(mask, length):

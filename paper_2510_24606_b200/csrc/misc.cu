@@ -63,9 +63,50 @@ __global__ void upsample_kernel(const double* __restrict__ sc, const int32_t* __
   out[e] = sc[(int64_t)ci * n + cj];
 }
 
+// softmax_row (core.py:69-77): e = exp(s - max s); e / sum e, fp64, one CTA
+// per row (block reductions of the max and of the sum).
+__global__ __launch_bounds__(256) void softmax_rows_kernel(const double* __restrict__ s,
+                                                           int64_t n, double* __restrict__ out) {
+  __shared__ double red[8];
+  const double* x = s + (int64_t)blockIdx.x * n;
+  double* y = out + (int64_t)blockIdx.x * n;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double m = -INFINITY;
+  for (int64_t i = threadIdx.x; i < n; i += 256) m = fmax(m, x[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) red[warp] = m;
+  __syncthreads();
+  m = red[0];
+#pragma unroll
+  for (int w = 1; w < 8; ++w) m = fmax(m, red[w]);
+  __syncthreads();
+  double t = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += 256) {
+    const double e = exp(x[i] - m);
+    y[i] = e;
+    t += e;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (lane == 0) red[warp] = t;
+  __syncthreads();
+  t = 0.0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) t += red[w];
+  for (int64_t i = threadIdx.x; i < n; i += 256) y[i] = y[i] / t;
+}
+
 }  // namespace dhsa
 
 using namespace dhsa;
+
+extern "C" int dhsa_softmax_rows(const double* scores, int rows, int64_t n, double* out,
+                                 dhsa_stream_t stream) {
+  DHSA_REQUIRE(scores && out && rows >= 1 && n >= 1, "dhsa_softmax_rows: bad arguments");
+  softmax_rows_kernel<<<rows, 256, 0, (cudaStream_t)stream>>>(scores, n, out);
+  return check_launch("dhsa_softmax_rows");
+}
 
 extern "C" int dhsa_upsample(const double* scores, const int32_t* bounds, int n, int L,
                              double* out, dhsa_stream_t stream) {

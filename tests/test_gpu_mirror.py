@@ -164,3 +164,21 @@ def test_topk_row_beyond_shared_memory(rng):
         want = O.token_topk(s, row, budget)
         assert np.array_equal(P.topk_row(s, row, budget), want), (row, budget)
 
+
+
+def test_softmax_row_reference_cases(rng):
+    """core.py:69-77 and the reference's own softmax tests (test_core.py:32-56)."""
+    for _ in range(20):
+        s = rng.standard_normal(int(rng.integers(1, 300))) * 10.0
+        e = np.exp(s - s.max())
+        np.testing.assert_allclose(P.softmax_row(s), e / e.sum(), atol=1e-14)
+        p = P.softmax_row(s)
+        assert abs(p.sum() - 1.0) < 1e-12 and np.all(p > 0)
+    s = rng.standard_normal(6)
+    np.testing.assert_allclose(P.softmax_row(s), P.softmax_row(s + 123.0), atol=1e-12)
+    np.testing.assert_allclose(P.softmax_row(np.zeros(5)), np.full(5, 0.2))
+    p = P.softmax_row(np.array([1000.0, 999.0]))
+    assert np.all(np.isfinite(p)) and abs(p.sum() - 1.0) < 1e-12
+    for bad in (np.zeros(0), np.zeros((2, 2)), np.array([1.0, np.inf])):
+        with pytest.raises(ValueError):
+            P.softmax_row(bad)
