@@ -198,8 +198,12 @@ int dhsa_sketch_build(const double* centroids, int64_t c_unit_stride, int D, int
                       dhsa_layout layout, void* sketch, int64_t sk_unit_stride,
                       float* sinfo, dhsa_stream_t stream);
 
-/* Bytes of global select scratch PER UNIT that dhsa_decode_step_bf16 needs
- * when a unit's chunks do not fit shared memory (0 = none needed). */
+/* Bytes of global select scratch PER UNIT for dhsa_decode_step_bf16 /
+ * dhsa_decode_candidates_bf16 with units of up to max_chunks chunks (20 B per
+ * chunk).  The scratch is required when a unit's chunks do not fit the
+ * generic select's shared memory (> 4,914 chunks) and lets the
+ * register-resident select run (it keeps its massive-tie fallback there);
+ * with NULL scratch the generic shared-memory select runs. */
 int64_t dhsa_sketch_select_scratch_size(int max_chunks);
 
 /* One decode step's K3 + K4 (+K2, + advance) for bf16 caches, D in {64,128},
@@ -210,7 +214,9 @@ int64_t dhsa_sketch_select_scratch_size(int max_chunks);
  *      += k_new and k/v appended at row plen+gen_count (masks.py:235), the
  *      certified walk -> tiles/ntiles exactly as dhsa_decode_select would
  *      produce from fp64 scores, and gen_count += 1 when `advance`.
- * scratch: U * dhsa_sketch_select_scratch_size bytes, or NULL when 0.
+ * scratch: U * dhsa_sketch_select_scratch_size bytes (or NULL, see there);
+ * approx rows: sc_stride >= max_chunks + 1 (a multiple of 4 lets the select
+ * read the scores as float4).
  * The select kernel is launched with programmatic stream serialization: its
  * prologue (query staging, generated-chunk update) overlaps the sketch stream
  * and it waits (griddepcontrol.wait) before reading the scores.

@@ -46,6 +46,8 @@ struct StreamArgs {
   int32_t* counters;  // [2]: pull counter, exits; zero at rest
   int32_t* ready;     // [items] or null (re-armed by the next step's first kernel)
   float scale_log2;
+  int spin_ns;              // back-off of the ready-flag wait
+  int l2_hint;              // evict-first L2 policy on the K/V stream
   unsigned long long* dbg;  // DHSA_DEBUG_TIMING (common.cuh)
 };
 
@@ -126,6 +128,10 @@ __global__ __launch_bounds__(192, 2) void attn_stream_kernel(const __grid_consta
       prefetch_tmap(&tmK);
       prefetch_tmap(&tmV);
     }
+    // K/V tiles are read once per step: evict-first (unless DHSA_L2_HINT=0)
+    uint64_t pol = 0;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+    if (a.l2_hint) pol = l2_policy_evict_first();
     const int head_pulls = a.head_items * a.nseg_big;
     const int total = head_pulls + (a.items - a.head_items) * a.nseg_small;
     int it = 0;
@@ -158,7 +164,7 @@ __global__ __launch_bounds__(192, 2) void attn_stream_kernel(const __grid_consta
       if (lane == 0) {
         if (a.ready) {
           int v;
-          while ((v = ld_acquire(a.ready + item)) < 1) __nanosleep(64);
+          while ((v = ld_acquire(a.ready + item)) < 1) __nanosleep(a.spin_ns);
           if (v < kReadyFinal && !(j < nseg - 1 && (j + 1) * S <= v - 1)) {
             spin_geq(a.ready + item, kReadyFinal);
             v = kReadyFinal;
@@ -197,8 +203,8 @@ __global__ __launch_bounds__(192, 2) void attn_stream_kernel(const __grid_consta
             mbar_expect_tx(&full_bar[st], STAGE_BYTES);
 #pragma unroll
             for (int b = 0; b < NB; ++b) {
-              tma_load_2d(dst + b * BOX, &tmK, &full_bar[st], b * 64, row);
-              tma_load_2d(dst + (NB + b) * BOX, &tmV, &full_bar[st], b * 64, row);
+              tma_load_2d_hint(dst + b * BOX, &tmK, &full_bar[st], b * 64, row, pol);
+              tma_load_2d_hint(dst + (NB + b) * BOX, &tmV, &full_bar[st], b * 64, row, pol);
             }
           }
           ++it;
@@ -397,6 +403,8 @@ static int launch_stream(const CUtensorMap& mk, const CUtensorMap& mv, StreamArg
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = a.ready ? 1 : 0;
+  if (const char* e = getenv("DHSA_NO_ATTN_PDL"))
+    if (atoi(e)) cfg.numAttrs = 0;
   e = cudaLaunchKernelEx(&cfg, kern, mk, mv, a);
   if (e != cudaSuccess) {
     set_error("dhsa_attn_stream: %s", cudaGetErrorString(e));
@@ -482,6 +490,10 @@ extern "C" int dhsa_attn_stream(const void* q, const void* k_cache, const void* 
   a.ready = ready;
   a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)D));
   if (const char* e = getenv("DHSA_DEBUG_TIMING")) a.dbg = (unsigned long long*)strtoull(e, nullptr, 0);
+  a.spin_ns = 64;
+  a.l2_hint = 1;
+  if (const char* e = getenv("DHSA_L2_HINT")) a.l2_hint = atoi(e);
+  if (const char* e = getenv("DHSA_SPIN_NS")) a.spin_ns = atoi(e);
   cudaStream_t s = (cudaStream_t)stream;
   int stages = 3;
   if (const char* e = getenv("DHSA_STREAM_STAGES")) stages = atoi(e);

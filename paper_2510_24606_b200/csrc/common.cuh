@@ -157,6 +157,23 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
       : "memory");
 }
+// The same with an L2 eviction-priority policy (createpolicy): streamed data
+// that is read once per step (K/V tiles, sketch slices) is marked evict-first
+// so the step's small, re-read state (approximate scores, tile lists, fp64
+// centroids of the re-scored chunks, flags, code) stays in L2.
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                                 int x, int y, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
 // 1-D bulk copy global -> shared (TMA engine), completion on an mbarrier.
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
                                           uint64_t* bar) {
@@ -177,6 +194,8 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
 // attention CTAs at kDbgAttn + 4 b (+1 first tile, +2 end).
 constexpr int kDbgSketch = 65536;
 constexpr int kDbgAttn = 131072;
+constexpr int kDbgSelectClk = 196608;
+constexpr int kDbgSketchPh = 229376;   // sketch CTAs: first q staged, first tile, last tile  // select CTAs: clock64() at the same phase points
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

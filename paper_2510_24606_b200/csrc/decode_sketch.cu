@@ -33,71 +33,14 @@
 // chunk slices, 8 consumer warps + 1 producer warp) -> sketch_select_kernel
 // (one CTA per kv unit: generated chunk in fp64 + state update, certified
 // walk, tiles for the attention kernel, gen_count += 1).
-#include "capi.cuh"
-#include "walk.cuh"
+#include "select2.cuh"
+#include "sketch_common.cuh"
 
-#include <cuda_fp16.h>
 #include <cstdlib>
-
-#ifndef SELECT_THREADS
-#define SELECT_THREADS 256
-#endif
 
 namespace dhsa {
 
-constexpr int kSelectThreads = SELECT_THREADS;
-constexpr int kSmallUncertain = 1024;
-
 constexpr int ilog2c(int x) { return x <= 1 ? 0 : 1 + ilog2c(x / 2); }
-
-struct SketchArgs {
-  const __nv_bfloat16* q;   // [U*G][D]
-  const __half* sketch;     // [U][sk_stride]
-  int64_t sk_stride;
-  const float* sinfo;       // [U][4]: scale exponent k (as float), cmax, dmax, unused
-  const double* cent;       // [U][c_stride] fp64 centroids (refinement)
-  int64_t c_stride;
-  double* gen_sum;          // [U][D]
-  int32_t* gen_count;       // [U]
-  const __nv_bfloat16* k_new;
-  const __nv_bfloat16* v_new;
-  __nv_bfloat16* kc;
-  __nv_bfloat16* vc;
-  int64_t cache_stride;
-  Layout lay;
-  float* approx;            // [items][sc_stride] scaled approximate scores
-  int64_t sc_stride;
-  int slices_per_unit;      // ceil(max_chunks / chunks_per_slice)
-  int64_t total_slices;
-  int64_t budget;
-  int tile_tokens;
-  int32_t* tiles;
-  int64_t tile_cap;
-  int32_t* ntiles;
-  unsigned char* gscratch;
-  int64_t gscratch_stride;
-  int smem_select;
-  int n_max;
-  int advance;
-  int32_t* ready;           // [items] select -> attention flags (zeroed by the sketch kernel) or null
-  int n_units;
-  int32_t* progress;        // [U] sketch -> select: consumer-warp slices done (zero at rest) or null
-  int early;                // publish the certainly-kept chunks' tiles before the refinement
-  unsigned long long* dbg;  // optional per-CTA phase timestamps (DHSA_DEBUG_TIMING)
-  // sequence-sharded split-KV mode (dhsa_decode_candidates_bf16): this shard
-  // holds global prompt chunks [chunk_offset, chunk_offset + nchunks); the
-  // tail shard also holds the generated chunk (global id total_chunks) and
-  // the newest token.  Instead of tiles, every chunk the local exact walk
-  // gives a positive take is written as a candidate record.
-  int split;
-  int32_t chunk_offset, total_chunks, total_prompt, owns_tail;
-  unsigned char* cand;      // [items][cand_stride] bytes: header + SplitCand[cand_cap]
-  int64_t cand_stride;
-  int cand_cap;
-};
-
-#define DBG_T(k) \
-  if (a.dbg && threadIdx.x == 0) a.dbg[blockIdx.x * 16 + (k)] = gtimer()
 
 template <int NV, int LG>
 __device__ __forceinline__ void transpose_reduce_f(float (&v)[NV], int lane) {
@@ -140,11 +83,6 @@ __device__ __forceinline__ int tr_index(int k, int glane) {
 // whole unit, each head scaled by a power of two 2^-kq so bf16 q is exact in
 // fp16.  4 consumer warps x 16 rows per 64-chunk slice; one producer thread
 // keeps kStages slices in flight with 2-D TMA loads.
-constexpr int kTcConsumers = 4;
-constexpr int kTcThreads = (kTcConsumers + 1) * 32;
-constexpr int kTcStages = 4;
-constexpr int kSliceRows = 64;
-
 template <int D, int G, int AGG>
 __global__ __launch_bounds__(kTcThreads) void sketch_score_kernel(
     const __grid_constant__ CUtensorMap tmS, SketchArgs a) {
@@ -175,7 +113,7 @@ __global__ __launch_bounds__(kTcThreads) void sketch_score_kernel(
     const int items = AGG == DHSA_AGG_NONE ? a.n_units * G : a.n_units;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < items; i += gridDim.x * blockDim.x)
       a.ready[i] = 0;
-    __threadfence();
+    if ((int64_t)blockIdx.x * blockDim.x < items) __threadfence();  // only the CTAs that wrote
   }
   __syncthreads();
   if (a.dbg && threadIdx.x == 0) a.dbg[kDbgSketch + 2 * blockIdx.x] = gtimer();
@@ -191,6 +129,9 @@ __global__ __launch_bounds__(kTcThreads) void sketch_score_kernel(
   if (warp == kTcConsumers) {
     if (lane == 0) {
       prefetch_tmap(&tmS);
+      uint64_t pol = 0;  // the sketch is read once per step: evict-first
+      asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+      if (a.l2_hint) pol = l2_policy_evict_first();
       int it = 0;
       for (int64_t sl = s_begin; sl < s_end; ++sl) {
         if (c0 < nc) {
@@ -199,7 +140,8 @@ __global__ __launch_bounds__(kTcThreads) void sketch_score_kernel(
           mbar_expect_tx(&full_bar[st], TILE);
           const int row = u * rows_per_unit + c0;
 #pragma unroll
-          for (int b = 0; b < NB; ++b) tma_load_2d(smem + st * STAGE + b * BOX, &tmS, &full_bar[st], b * 64, row);
+          for (int b = 0; b < NB; ++b)
+            tma_load_2d_hint(smem + st * STAGE + b * BOX, &tmS, &full_bar[st], b * 64, row, pol);
           ++it;
         }
         c0 += kSliceRows;
@@ -220,10 +162,9 @@ __global__ __launch_bounds__(kTcThreads) void sketch_score_kernel(
   auto publish = [&](int pu, int pn) {
     if (!a.progress || pu < 0 || pn == 0) return;
     __syncwarp();
-    if (lane == 0) {
-      __threadfence();
-      atomicAdd(a.progress + pu, pn);
-    }
+    // release-add: the warp's score stores (ordered by the __syncwarp) are
+    // visible before the count the select acquires
+    if (lane == 0) red_add_release(a.progress + pu, pn);
   };
   const int hcol = lane >> 2;  // B column (head) owned for the fragment
   uint32_t qb[KS][2];
@@ -275,7 +216,9 @@ __global__ __launch_bounds__(kTcThreads) void sketch_score_kernel(
       kq1 = __shfl_sync(0xffffffffu, kq, 4 * (2 * (lane & 3) + 1));
     }
     const int st = it % kTcStages;
+    if (a.dbg && threadIdx.x == 0 && it == 0) a.dbg[kDbgSketchPh + 4 * blockIdx.x] = gtimer();
     mbar_wait(&full_bar[st], (it / kTcStages) & 1);
+    if (a.dbg && threadIdx.x == 0 && it == 0) a.dbg[kDbgSketchPh + 4 * blockIdx.x + 1] = gtimer();
     const uint32_t base = smem_u32(smem + st * STAGE);
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -324,37 +267,9 @@ __global__ __launch_bounds__(kTcThreads) void sketch_score_kernel(
     }
     ++pend_n;  // slices of unit pend_u this warp has scored, published per unit
   }
+  if (a.dbg && threadIdx.x == 0) a.dbg[kDbgSketchPh + 4 * blockIdx.x + 2] = gtimer();
   publish(pend_u, pend_n);
   if (a.dbg && threadIdx.x == 0) a.dbg[kDbgSketch + 2 * blockIdx.x + 1] = gtimer();
-}
-
-// --------------------------------------------------------------- selection --
-struct UnitChunks {
-  Layout lay;
-  int u, nc, g, P;
-  __device__ void chunk(int c, int& lo, int& len) const {
-    if (c < nc) {
-      if (lay.bounds) {
-        int hi;
-        lay.chunk(u, c, lo, hi);
-        len = hi - lo;
-      } else {  // static grid: arithmetic only (P is cached in the struct)
-        lo = c * lay.block;
-        len = min(lay.block, P - lo);
-      }
-    } else {
-      lo = P;
-      len = g;
-    }
-  }
-};
-
-template <int G, int AGG>
-__device__ __forceinline__ double agg_d(const double* v, int nh) {
-  double s = v[0];
-  for (int h = 1; h < nh; ++h) s = (AGG == DHSA_AGG_MAX) ? fmax(s, v[h]) : s + v[h];
-  if (AGG == DHSA_AGG_MEAN && nh > 1) s = s / (double)nh;
-  return s;
 }
 
 // Weighted cut of the approximate scores by a value histogram: one min/max
@@ -363,7 +278,6 @@ __device__ __forceinline__ double agg_d(const double* v, int nh) {
 // W(bin > b*) < R <= W(bin >= b*) for bin(x) = clamp(floor((x - vmin) *
 // bscale), 0, kHistBins - 1), which is monotone in x.  Requires 0 < R <
 // total weight.  Replaces a 4-pass 8-bit radix select (~7 us -> ~2 us).
-constexpr int kHistBins = 1024;
 __device__ __forceinline__ int hpad(int b) { return b + (b >> 5); }  // bank-conflict-free scan
 template <int NT>
 struct HistShared {
@@ -438,63 +352,6 @@ __device__ int hist_threshold(const uint32_t* ak, const int32_t* lens, int n, ui
   return __shfl_sync(0xffffffffu, bstar, f < 0 ? 0 : f);
 }
 
-// Split-KV: every chunk with a positive local take (takes in lens[]) becomes a
-// candidate record with its exact fp64 score (the same arithmetic as the
-// re-scoring above), global chunk id, full length and local start token.
-// The global walk (splitkv.cu) over the candidates of all shards then equals
-// the unsharded walk: a chunk with a positive global take has fewer than R
-// tokens ranked above it globally, hence locally, so it is a local candidate.
-template <int D, int G, int AGG, int NT>
-__device__ void emit_candidates(const SketchArgs& a, const UnitChunks& uc, const int32_t* takes,
-                                int32_t* list, int n, int s, const double (*qd)[D], int h0, int nh,
-                                double gex, int u) {
-  constexpr int NW = NT / 32;
-  __shared__ int s_ncand;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_ncand = 0;
-  __syncthreads();
-  for (int c = tid; c < n; c += NT)
-    if (takes[c] > 0) list[atomicAdd(&s_ncand, 1)] = c;
-  __syncthreads();
-  const int nc = s_ncand;
-  unsigned char* row = a.cand + (int64_t)s * a.cand_stride;
-  SplitCand* rec = reinterpret_cast<SplitCand*>(row) + 1;
-  for (int i = warp; i < nc && i < a.cand_cap; i += NW) {
-    const int c = list[i];
-    int lo, len;
-    uc.chunk(c, lo, len);
-    double ex;
-    if (c < uc.nc) {
-      const double* crow = a.cent + (int64_t)u * a.c_stride + (int64_t)c * D;
-      double part[G];
-#pragma unroll
-      for (int h = 0; h < G; ++h) part[h] = 0.0;
-#pragma unroll
-      for (int d = lane; d < D; d += 32) {
-        const double cv = crow[d];
-#pragma unroll
-        for (int h = 0; h < G; ++h) part[h] = fma(qd[h][d], cv, part[h]);
-      }
-#pragma unroll
-      for (int h = 0; h < G; ++h) part[h] = warp_sum(part[h]);
-      ex = agg_d<G, AGG>(part + h0, nh);
-    } else {
-      ex = gex;
-    }
-    if (lane == 0) {
-      SplitCand r;
-      r.score = ex;
-      r.gid = c < uc.nc ? a.chunk_offset + c : a.total_chunks;
-      r.len = len;
-      r.lo = lo;
-      r.pad = 0;
-      rec[i] = r;
-    }
-  }
-  if (tid == 0) reinterpret_cast<int32_t*>(row)[0] = nc <= a.cand_cap ? nc : -1;
-  __syncthreads();
-}
-
 template <int D, int G, int AGG, int NT>
 __global__ __launch_bounds__(NT) void sketch_select_kernel(SketchArgs a) {
   constexpr int NW = NT / 32;
@@ -515,79 +372,8 @@ __global__ __launch_bounds__(NT) void sketch_select_kernel(SketchArgs a) {
 
   pdl_trigger();  // the attention kernel may launch once every select CTA is resident
   DBG_T(0);
-  // ---- prologue: every global load of the step issued before one barrier ----
-  for (int i = tid; i < G * D; i += NT)
-    qd[i / D][i % D] = to_f64(a.q[(int64_t)u * G * D + i]);
-  const int g = a.gen_count[u];
-  const int gl = (a.split && !a.owns_tail) ? 0 : g;  // generated tokens held by this shard
-  constexpr int DV = D / 32;
-  static_assert(NW >= 2, "select needs >= 2 warps");
-  if (warp < NW - 1) {  // query norms (certified bound), warps 0 .. NW-2
-    for (int h = warp; h < G; h += NW - 1) {
-      double t = 0.0;
-#pragma unroll
-      for (int v = 0; v < DV; ++v) {
-        const double x = to_f64(a.q[(int64_t)(u * G + h) * D + lane + 32 * v]);
-        t = fma(x, x, t);
-      }
-      t = warp_sum(t);
-      if (lane == 0) s_qn[h] = sqrt(t) * (1.0 + 1e-12);
-    }
-  } else {
-    // generated chunk, exact fp64 (masks.py:161), then the state update
-    double* gs = a.gen_sum + (int64_t)u * D;
-    double gv[DV], qv[G][DV];
-    __nv_bfloat16 kv[DV], vv[DV];
-#pragma unroll
-    for (int v = 0; v < DV; ++v) {
-      const int d = lane + 32 * v;
-      gv[v] = gs[d];
-      if (a.k_new) kv[v] = a.k_new[(int64_t)u * D + d];
-      if (a.v_new) vv[v] = a.v_new[(int64_t)u * D + d];
-#pragma unroll
-      for (int h = 0; h < G; ++h) qv[h][v] = to_f64(a.q[(int64_t)(u * G + h) * D + d]);
-    }
-    double part[G];
-#pragma unroll
-    for (int h = 0; h < G; ++h) part[h] = 0.0;
-    if (gl >= 1) {
-      const double rs = __dsqrt_rn((double)gl);
-#pragma unroll
-      for (int v = 0; v < DV; ++v) {
-        const double cg = __ddiv_rn(gv[v], rs);
-#pragma unroll
-        for (int h = 0; h < G; ++h) part[h] = fma(qv[h][v], cg, part[h]);
-      }
-#pragma unroll
-      for (int h = 0; h < G; ++h) part[h] = warp_sum(part[h]);
-    }
-    if (lane == 0)
-#pragma unroll
-      for (int h = 0; h < G; ++h) s_gen[h] = part[h];
-    if (a.k_new) {  // masks.py:235: after the read above; k/v appended at row P+g
-      const int64_t pos = (int64_t)(a.lay.prompt_len(u) + gl) * D;
-#pragma unroll
-      for (int v = 0; v < DV; ++v) {
-        const int d = lane + 32 * v;
-        gs[d] = __dadd_rn(gv[v], to_f64(kv[v]));
-        if (a.kc) a.kc[(int64_t)u * a.cache_stride + pos + d] = kv[v];
-        if (a.vc) a.vc[(int64_t)u * a.cache_stride + pos + d] = vv[v];
-      }
-    }
-  }
-  // the unit's approximate scores are complete once every consumer warp of
-  // every slice of the unit has published (progress), or - without progress
-  // counters - once the whole score grid has finished
-  if (a.progress) {
-    if (tid == 0) {
-      const int slices = (a.lay.num_chunks(u) + kSliceRows - 1) / kSliceRows;
-      spin_geq(a.progress + u, kTcConsumers * slices);
-      a.progress[u] = 0;  // re-arm: the next step's stream starts after this grid
-    }
-  } else {
-    pdl_wait();
-  }
-  __syncthreads();
+  int g, gl;
+  select_prologue<D, G, NT>(a, u, qd, s_qn, s_gen, g, gl);
   DBG_T(1);
 
   UnitChunks uc{a.lay, u, a.lay.num_chunks(u), gl, a.lay.prompt_len(u)};
@@ -706,10 +492,9 @@ __global__ __launch_bounds__(NT) void sketch_select_kernel(SketchArgs a) {
           }
           base = total;
           __syncthreads();
-          if (tid == 0 && base > 0) {
-            __threadfence();
-            st_release(a.ready + s, 1 + base);
-          }
+          // the barrier orders every thread's tile stores before thread 0's
+          // release (cumulative): the attention acquires the flag
+          if (tid == 0 && base > 0) st_release(a.ready + s, 1 + base);
         }
       }
       DBG_T(4);
@@ -790,7 +575,6 @@ __global__ __launch_bounds__(NT) void sketch_select_kernel(SketchArgs a) {
   if (tid == 0) {
     if (a.advance) a.gen_count[u] = g + 1;  // masks.py:236
     if (a.ready) {  // tiles, running sum and appended k/v are published together
-      __threadfence();
       for (int it = 0; it < nitems; ++it)
         st_release(a.ready + (AGG == DHSA_AGG_NONE ? u * G + it : u), kReadyFinal);
     }
@@ -873,11 +657,16 @@ static int launch_step(const SketchArgs& a, int U, size_t sel_smem, cudaStream_t
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, score, kTcThreads, ring);
+  if (const char* e = getenv("DHSA_SKETCH_CTAS_PER_SM")) per_sm = atoi(e) > 0 ? atoi(e) : per_sm;
   int64_t grid = (int64_t)sms * (per_sm < 1 ? 1 : per_sm);
   if (grid > a.total_slices) grid = a.total_slices;
   score<<<(unsigned)grid, kTcThreads, ring, s>>>(tm, a);
   rc = check_launch("dhsa_decode_step_bf16(score)");
   if (rc) return rc;
+  {
+    int rc2 = 0;
+    if (launch_select2<D, G, AGG>(a, U, s, &rc2)) return rc2;
+  }
   // a wider CTA for very long units (e.g. 16K chunks in one split-KV shard)
   auto sel = a.n_max > 4096 ? sketch_select_kernel<D, G, AGG, 1024>
                             : sketch_select_kernel<D, G, AGG, kSelectThreads>;
@@ -936,9 +725,12 @@ using namespace dhsa;
 
 constexpr int64_t kSelectSmemLimit = 96 * 1024;
 
+static int64_t select_scratch_per_unit(int max_chunks) {
+  return (((int64_t)max_chunks + 1) * (8 + 4 + 4 + 4) + 15) / 16 * 16;
+}
+
 extern "C" int64_t dhsa_sketch_select_scratch_size(int max_chunks) {
-  const int64_t per_unit = ((int64_t)max_chunks + 1) * (8 + 4 + 4 + 4);
-  return per_unit <= kSelectSmemLimit ? 0 : (per_unit + 15) / 16 * 16;
+  return select_scratch_per_unit(max_chunks);
 }
 
 extern "C" int dhsa_sketch_build(const double* centroids, int64_t c_unit_stride, int D, int U,
@@ -1041,17 +833,23 @@ static int decode_step_impl(
     a.early = 0;
   }
   if (const char* e = getenv("DHSA_DEBUG_TIMING")) a.dbg = (unsigned long long*)strtoull(e, nullptr, 0);
-  const int64_t need = dhsa_sketch_select_scratch_size(layout.max_chunks);
+  a.l2_hint = 1;
+  if (const char* e = getenv("DHSA_L2_HINT")) a.l2_hint = atoi(e);
+  a.reps = 1;
+  if (const char* e = getenv("DHSA_SELECT_REPS")) a.reps = atoi(e) > 0 ? atoi(e) : 1;
+  const int64_t need = select_scratch_per_unit(layout.max_chunks);
   size_t smem = 0;
-  if (need == 0) {
+  if (scratch) {
+    a.gscratch = (unsigned char*)scratch;
+    a.gscratch_stride = need;
+  }
+  if (need <= kSelectSmemLimit) {  // the generic select keeps its arrays in shared memory
     a.smem_select = 1;
     smem = (size_t)a.n_max * (8 + 4 + 4 + 4);
   } else {
     DHSA_REQUIRE(scratch, "dhsa_decode_step_bf16: %lld bytes of select scratch per unit required",
                  (long long)need);
     a.smem_select = 0;
-    a.gscratch = (unsigned char*)scratch;
-    a.gscratch_stride = need;
   }
   cudaStream_t s = (cudaStream_t)stream;
   if (D == 128) return dispatch_agg<128>(agg, G, a, U, smem, s);

@@ -124,12 +124,13 @@ class SparseDecoder:
             self.sketch = torch.zeros(batch, kv_heads, self.nc_cap, head_dim, dtype=torch.float16,
                                       **kw)
             self.sinfo = torch.zeros(self.U, 4, dtype=torch.float32, **kw)
-            self.approx = torch.empty(self.items, self.nc_cap + 1, dtype=torch.float32, **kw)
+            # rows padded to a multiple of 4 floats (the select reads float4)
+            self.sc_stride = (self.nc_cap + 1 + 3) // 4 * 4
+            self.approx = torch.empty(self.items, self.sc_stride, dtype=torch.float32, **kw)
             self.ready = torch.zeros(self.items, dtype=torch.int32, **kw)
             self.progress = torch.zeros(self.U, dtype=torch.int32, **kw)
             per_unit = _lib.load().dhsa_sketch_select_scratch_size(self.nc_cap)
-            self.scratch = (torch.empty(self.U * per_unit, dtype=torch.uint8, **kw)
-                            if per_unit > 0 else None)
+            self.scratch = torch.empty(self.U * per_unit, dtype=torch.uint8, **kw)
         # fp64 scoring: the select kernel's global scratch for very long units
         per_row = _lib.load().dhsa_select_scratch_size(self.nc_cap + 1)
         self.sel_scratch = (torch.empty(per_row * self.items, dtype=torch.uint8, **kw)
@@ -294,7 +295,7 @@ class SparseDecoder:
                           _lib.ptr(self.v_cache), self.L_cap * self.D, lay, self.U, self.G,
                           self.D, agg, self.budget, self.tile, _lib.ptr(self.tiles),
                           self.tile_cap, _lib.ptr(self.ntiles), _lib.ptr(self.approx),
-                          self.nc_cap + 1, _lib.ptr(self.scratch), _lib.ptr(self.ready), 1,
+                          self.sc_stride, _lib.ptr(self.scratch), _lib.ptr(self.ready), 1,
                           _lib.ptr(self.progress), st)
             return [("score_select", fused), attn]
 

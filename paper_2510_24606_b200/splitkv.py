@@ -195,7 +195,7 @@ class SplitKVShard:
                   _lib.ptr(d.k_cache) if tail else 0, _lib.ptr(d.v_cache) if tail else 0,
                   d.L_cap * d.D, d._layout(), d.U, d.G, d.D, _lib.AGG[d.agg], d.budget,
                   self.spec, _lib.ptr(self.cand), self.cand_stride, self.cap,
-                  _lib.ptr(d.approx), d.nc_cap + 1, _lib.ptr(d.scratch), _lib.ptr(d.progress),
+                  _lib.ptr(d.approx), d.sc_stride, _lib.ptr(d.scratch), _lib.ptr(d.progress),
                   st)
 
     def select(self, gathered=None, stream=None):

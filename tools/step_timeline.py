@@ -82,10 +82,29 @@ def show(name, col):
 print(f"graph replay (events): {e0.elapsed_time(e1) * 1e3:.1f} us")
 show("sketch CTA start", sk[:, 0])
 show("sketch CTA end", sk[:, 1])
+ph = t[229376:229376 + 4 * 1024].reshape(-1, 4)[: len(sk)]
+show("sketch q staged", ph[:, 0])
+show("sketch first tile", ph[:, 1])
+show("sketch last tile", ph[:, 2])
 for k_, n in [(0, "select start"), (1, "select after pdl_wait"), (2, "select keys loaded"),
               (3, "select after threshold"), (4, "select classified"), (5, "select rescored"),
               (6, "select exact walk"), (7, "select emitted"), (8, "select end")]:
     show(n, sel[:, k_])
+clk = t[196608:196608 + dec.U * 16].reshape(dec.U, 16)
+mhz = float(os.environ.get("TL_MHZ", 1965))
+names = {0: "start", 1: "prologue+wait", 2: "keys", 3: "threshold", 9: "classified", 10: "phaseA tiles",
+         11: "phaseA fence+flag", 4: "(phase A done)", 5: "rescored", 6: "exact walk", 7: "emitted",
+         8: "end"}
+order = [0, 1, 2, 3, 9, 10, 11, 4, 5, 6, 7, 8]
+prev = None
+print("select phase durations (clock64, median over units, us at %.0f MHz):" % mhz)
+for k_ in order:
+    col = clk[:, k_]
+    if prev is not None and (col > 0).all() and (clk[:, prev] > 0).all():
+        d = (col - clk[:, prev]) / mhz
+        print(f"  {names[prev]:>18s} -> {names[k_]:<18s} med {np.median(d):7.2f}  max {d.max():7.2f}")
+    if (col > 0).all():
+        prev = k_
 show("attn CTA start", at[:, 0])
 show("attn first tile", at[:, 1])
 show("attn CTA end", at[:, 2])
