@@ -74,8 +74,10 @@ __device__ __forceinline__ int warp_incl_scan(int x, int lane) {
 // order, starting at tile index `base`; one warp (lane l owns words 3l..3l+2).
 // Returns the tile count (uniform over the warp).
 static __device__ __forceinline__ int s3_emit_whole(const UnitChunks& uc, const uint32_t* words,
-                                          int tile_tokens, int32_t* out, int64_t cap, int base) {
+                                          int tile_tokens, int32_t* out, int64_t cap, int base,
+                                          unsigned long long* dbg = nullptr) {
   const int lane = threadIdx.x & 31;
+  if (dbg && lane == 0) dbg[11] = clock64();
   uint32_t w[kS3WPL];
   int cnt = 0;
 #pragma unroll
@@ -90,8 +92,10 @@ static __device__ __forceinline__ int s3_emit_whole(const UnitChunks& uc, const 
       cnt += ntiles_of(len, tile_tokens);
     }
   }
+  if (dbg && lane == 0) dbg[12] = clock64();
   const int incl = warp_incl_scan(cnt, lane);
   int off = base + incl - cnt;
+  if (dbg && lane == 0) dbg[13] = clock64();
 #pragma unroll
   for (int j = 0; j < kS3WPL; ++j) {
     uint32_t m = w[j];
@@ -107,6 +111,7 @@ static __device__ __forceinline__ int s3_emit_whole(const UnitChunks& uc, const 
         }
     }
   }
+  if (dbg && lane == 0) dbg[14] = clock64();
   return __shfl_sync(0xffffffffu, incl, 31);
 }
 
@@ -298,7 +303,8 @@ __global__ __launch_bounds__(kS3Threads, 3) void sketch_select3_kernel(SketchArg
     DBG_T(9);
     if (warp == 0) {
       // ---- the chunks kept whole: tiles in chunk order, published early ----
-      const int base = s3_emit_whole(uc, inbits, a.tile_tokens, out, a.tile_cap, 0);
+      const int base = s3_emit_whole(uc, inbits, a.tile_tokens, out, a.tile_cap, 0,
+                                     a.dbg ? a.dbg + kDbgSelectClk + blockIdx.x * 16 : nullptr);
       __syncwarp();  // the warp's tile stores, before lane 0's (cumulative) release
       if (lane == 0) {
         s_base = base;

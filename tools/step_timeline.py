@@ -92,10 +92,11 @@ for k_, n in [(0, "select start"), (1, "select after pdl_wait"), (2, "select key
     show(n, sel[:, k_])
 clk = t[196608:196608 + dec.U * 16].reshape(dec.U, 16)
 mhz = float(os.environ.get("TL_MHZ", 1965))
-names = {0: "start", 1: "prologue+wait", 2: "keys", 3: "threshold", 9: "classified", 10: "phaseA tiles",
-         11: "phaseA fence+flag", 4: "(phase A done)", 5: "rescored", 6: "exact walk", 7: "emitted",
+names = {0: "start", 1: "prologue+wait", 2: "keys", 3: "threshold", 9: "classified",
+         11: "emitA start", 12: "emitA counted", 13: "emitA scanned", 14: "emitA written",
+         10: "phaseA tiles", 4: "(phase A done)", 5: "rescored", 6: "exact walk", 7: "emitted",
          8: "end"}
-order = [0, 1, 2, 3, 9, 10, 11, 4, 5, 6, 7, 8]
+order = [0, 1, 2, 3, 9, 11, 12, 13, 14, 10, 4, 5, 6, 7, 8]
 prev = None
 print("select phase durations (clock64, median over units, us at %.0f MHz):" % mhz)
 for k_ in order:
