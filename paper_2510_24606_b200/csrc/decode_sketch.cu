@@ -42,6 +42,16 @@ namespace dhsa {
 
 constexpr int ilog2c(int x) { return x <= 1 ? 0 : 1 + ilog2c(x / 2); }
 
+// 2^k as a float for a normal-range exponent, else 0 (the caller falls back
+// to ldexpf); x * 2^k is then exact unless it under/overflows, exactly as
+// ldexpf(x, k) would round
+__device__ __forceinline__ float pow2f(int k) {
+  return (k > -127 && k < 128) ? __int_as_float((127 + k) << 23) : 0.f;
+}
+__device__ __forceinline__ float scale2(float x, int k, float p) {
+  return p != 0.f ? x * p : ldexpf(x, k);
+}
+
 template <int NV, int LG>
 __device__ __forceinline__ void transpose_reduce_f(float (&v)[NV], int lane) {
   int n = NV;
@@ -169,6 +179,7 @@ __global__ __launch_bounds__(kTcThreads) void sketch_score_kernel(
   const int hcol = lane >> 2;  // B column (head) owned for the fragment
   uint32_t qb[KS][2];
   int kq0 = 0, kq1 = 0;        // scale exponents of the two heads in this lane's C columns
+  float p0 = 1.f, p1 = 1.f;     // 2^kq0, 2^kq1 (0 when out of the normal range: ldexpf)
   int cur_u = -1;
   const int mi = lane >> 3, r8 = lane & 7;
   const int arow = warp * 16 + (mi & 1) * 8 + r8;  // A row addressed by this lane
@@ -204,16 +215,20 @@ __global__ __launch_bounds__(kTcThreads) void sketch_score_kernel(
       amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
       amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 2));
       const int kq = amax > 0.f ? ilogbf(amax) + 1 - 14 : 0;  // max|q| 2^-kq < 2^14
+      // 2^-kq: an exact power-of-two multiply (ldexpf only outside the normal range)
+      const float qs = (kq > -127 && kq < 127) ? __int_as_float((127 - kq) << 23) : ldexpf(1.f, -kq);
 #pragma unroll
       for (int ks = 0; ks < KS; ++ks) {
-        const __half2 lo = __floats2half2_rn(ldexpf(qv[ks][0], -kq), ldexpf(qv[ks][1], -kq));
-        const __half2 hi = __floats2half2_rn(ldexpf(qv[ks][2], -kq), ldexpf(qv[ks][3], -kq));
+        const __half2 lo = __floats2half2_rn(qv[ks][0] * qs, qv[ks][1] * qs);
+        const __half2 hi = __floats2half2_rn(qv[ks][2] * qs, qv[ks][3] * qs);
         qb[ks][0] = *reinterpret_cast<const uint32_t*>(&lo);
         qb[ks][1] = *reinterpret_cast<const uint32_t*>(&hi);
       }
       // C columns of this lane are heads 2(lane&3), 2(lane&3)+1: fetch their exponents
       kq0 = __shfl_sync(0xffffffffu, kq, 4 * (2 * (lane & 3)));
       kq1 = __shfl_sync(0xffffffffu, kq, 4 * (2 * (lane & 3) + 1));
+      p0 = pow2f(kq0);
+      p1 = pow2f(kq1);
     }
     const int st = it % kTcStages;
     if (a.dbg && threadIdx.x == 0 && it == 0) a.dbg[kDbgSketchPh + 4 * blockIdx.x] = gtimer();
@@ -235,10 +250,10 @@ __global__ __launch_bounds__(kTcThreads) void sketch_score_kernel(
     // acc[0..1]: row warp*16 + lane/4, heads 2(lane&3)+{0,1}; acc[2..3]: row + 8
     const int h0 = 2 * (lane & 3);
     float v[4];
-    v[0] = h0 < G ? ldexpf(acc[0], kq0) : -INFINITY;
-    v[1] = h0 + 1 < G ? ldexpf(acc[1], kq1) : -INFINITY;
-    v[2] = h0 < G ? ldexpf(acc[2], kq0) : -INFINITY;
-    v[3] = h0 + 1 < G ? ldexpf(acc[3], kq1) : -INFINITY;
+    v[0] = h0 < G ? scale2(acc[0], kq0, p0) : -INFINITY;
+    v[1] = h0 + 1 < G ? scale2(acc[1], kq1, p1) : -INFINITY;
+    v[2] = h0 < G ? scale2(acc[2], kq0, p0) : -INFINITY;
+    v[3] = h0 + 1 < G ? scale2(acc[3], kq1, p1) : -INFINITY;
     const int r0 = warp * 16 + (lane >> 2);
     if constexpr (AGG == DHSA_AGG_NONE) {
 #pragma unroll
