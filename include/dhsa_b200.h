@@ -409,6 +409,27 @@ int dhsa_predictor_forward(const double* keys, int L, int d, int window, int hea
                            const double* b1, const double* w2, double b2, void* workspace,
                            double* probs, dhsa_stream_t stream);
 
+/* Mask-quality metrics of the reference harness, fp64 (harness.py:265-306,
+ * core.py:122-152), for the drop-in harness API:
+ * dhsa_causal_probs   causal_attention_probs (core.py:122-136): out [L][L],
+ *                      row i = softmax(q_i . k_j / sqrt(d)) over j <= i, 0 above;
+ * dhsa_mask_recall     attention_mass_recall's per-row fraction (harness.py:
+ *                      265-276): frac[i] = sum P[i, row_i] / sum P[i, 0..i] (0 if
+ *                      the total is 0); rows as CSR (row_ptr [L+1] int64, idx int32);
+ * dhsa_row_cosine      cosine_similarity (core.py:139-152) of `rows` row pairs;
+ * dhsa_mean            deterministic mean of n values (out[0]);
+ * dhsa_stack_reduce    aggregated_chunk_scores' max / mean over H stacked
+ *                      [n] score arrays (harness.py:302-306). */
+int dhsa_causal_probs(const double* q, const double* k, int L, int d, double* out,
+                      dhsa_stream_t stream);
+int dhsa_mask_recall(const double* probs, int64_t ld, int L, const int64_t* row_ptr,
+                     const int32_t* idx, double* frac, dhsa_stream_t stream);
+int dhsa_row_cosine(const double* a, const double* b, int64_t rows, int d, double* out,
+                    dhsa_stream_t stream);
+int dhsa_mean(const double* x, int64_t n, double* out, dhsa_stream_t stream);
+int dhsa_stack_reduce(const double* x, int H, int64_t n, int agg, double* out,
+                      dhsa_stream_t stream);
+
 /* softmax_row (core.py:69-77) of `rows` fp64 rows of n scores each:
  * out = exp(s - max s) / sum(exp(s - max s)), per row. */
 int dhsa_softmax_rows(const double* scores, int rows, int64_t n, double* out,

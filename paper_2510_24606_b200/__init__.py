@@ -10,22 +10,25 @@ device is missing.
 """
 
 from .chunking import check_boundaries, extend_for_decode, nms_boundaries, static_boundaries
-from .core import TokenSequence, dense_attention, softmax_row
+from .core import TokenSequence, causal_attention_probs, cosine_similarity, dense_attention, \
+    softmax_row
 from .chunk_repr import ChunkReps, aggregate_chunk, aggregate_rows, build_chunk_reps, \
     chunk_similarity
-from . import predictor, serialization
+from . import harness, predictor, serialization
 from .masks import CostCounters, DecodeSession, SparsityMask, decode_mask_row, \
     mask_from_chunk_scores, prefill_mask, topk_row, upsample
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "TokenSequence", "softmax_row", "dense_attention",
+    "TokenSequence", "softmax_row", "dense_attention", "causal_attention_probs",
+    "cosine_similarity",
     "check_boundaries", "static_boundaries", "nms_boundaries", "extend_for_decode",
     "ChunkReps", "aggregate_chunk", "aggregate_rows", "build_chunk_reps", "chunk_similarity",
     "CostCounters", "SparsityMask", "upsample", "topk_row", "mask_from_chunk_scores",
     "prefill_mask", "decode_mask_row", "DecodeSession",
     "SparseDecoder", "SparsePrefill", "SplitKVShard", "SplitKVGroup", "predictor",
+    "harness",
 ]
 
 

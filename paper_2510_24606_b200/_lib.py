@@ -74,6 +74,11 @@ _SIGS = {
                                    vp, C.c_int64, vp, vp, vp]),
     "dhsa_upsample": (C.c_int, [vp, vp, C.c_int, C.c_int, vp, vp]),
     "dhsa_softmax_rows": (C.c_int, [vp, C.c_int, C.c_int64, vp, vp]),
+    "dhsa_causal_probs": (C.c_int, [vp, vp, C.c_int, C.c_int, vp, vp]),
+    "dhsa_mask_recall": (C.c_int, [vp, C.c_int64, C.c_int, vp, vp, vp, vp]),
+    "dhsa_row_cosine": (C.c_int, [vp, vp, C.c_int64, C.c_int, vp, vp]),
+    "dhsa_mean": (C.c_int, [vp, C.c_int64, vp, vp]),
+    "dhsa_stack_reduce": (C.c_int, [vp, C.c_int, C.c_int64, C.c_int, vp, vp]),
     "dhsa_sketch_build": (C.c_int, [vp, C.c_int64, C.c_int, C.c_int, Layout, vp, C.c_int64, vp,
                                     vp]),
     "dhsa_sketch_select_scratch_size": (C.c_int64, [C.c_int]),

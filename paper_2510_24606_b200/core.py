@@ -2,7 +2,8 @@
 (masked) causal attention ``dense_attention``.
 
 Reference: core.py:35-66 (TokenSequence), core.py:69-77 (softmax_row),
-core.py:80-119 (_mask_rows, dense_attention).  The attention runs on the GPU through ``dhsa_attn`` in
+core.py:80-119 (_mask_rows, dense_attention), core.py:122-152
+(causal_attention_probs, cosine_similarity).  The attention runs on the GPU through ``dhsa_attn`` in
 fp64 (DFMA, online softmax), so outputs agree with the float64 reference to
 ~1e-15; masks are validated on the host with the reference's error messages.
 """
@@ -15,7 +16,8 @@ import numpy as np
 
 from . import _dev, _lib
 
-__all__ = ["TokenSequence", "softmax_row", "dense_attention"]
+__all__ = ["TokenSequence", "softmax_row", "dense_attention", "causal_attention_probs",
+           "cosine_similarity"]
 
 
 def _matrix(x, name):
@@ -137,7 +139,46 @@ def dense_attention(seq: TokenSequence, mask=None) -> np.ndarray:
         rows = [np.arange(i + 1) for i in range(L)]
     else:
         rows = _validated_rows(mask, L)
+    return _dev.host(attention_dev(seq, rows))
+
+
+def attention_dev(seq: TokenSequence, rows):
+    """fp64 masked causal attention of validated index rows -> device [L, d]."""
     tiles, ntiles = rows_to_tiles(rows)
     q, k, v = _dev.f64(seq.queries), _dev.f64(seq.keys), _dev.f64(seq.values)
-    out = attend_tiles(q, k, v, _dev.i32(tiles), _dev.i32(ntiles))
-    return _dev.host(out)
+    return attend_tiles(q, k, v, _dev.i32(tiles), _dev.i32(ntiles))
+
+
+def causal_probs_dev(seq: TokenSequence):
+    """Device [L, L] fp64 causal softmax probabilities (dhsa_causal_probs)."""
+    L, d = seq.queries.shape
+    q, k = _dev.f64(seq.queries), _dev.f64(seq.keys)
+    out = _dev.empty((L, L))
+    _lib.call("dhsa_causal_probs", _lib.ptr(q), _lib.ptr(k), L, d, _lib.ptr(out), _dev.stream())
+    return out
+
+
+def causal_attention_probs(seq: TokenSequence) -> np.ndarray:
+    """Full causal attention probability matrix, rows summing to 1 and zeros
+    above the diagonal (core.py:122-136), computed in fp64 on the device."""
+    return _dev.host(causal_probs_dev(seq))
+
+
+def cosine_rows_dev(a, b):
+    """Per-row cosine of two device [rows, d] fp64 tensors -> device [rows]."""
+    rows, d = a.shape
+    out = _dev.empty((rows,))
+    _lib.call("dhsa_row_cosine", _lib.ptr(a), _lib.ptr(b), rows, d, _lib.ptr(out), _dev.stream())
+    return out
+
+
+def cosine_similarity(a, b) -> float:
+    """Cosine of two vectors; 0.0 when either has zero norm, clamped to
+    [-1, 1] (core.py:139-152); computed on the device (dhsa_row_cosine)."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    if a.shape != b.shape or a.ndim != 1:
+        raise ValueError("cosine_similarity expects two equal-length vectors")
+    if a.size == 0:
+        return 0.0
+    return float(_dev.host(cosine_rows_dev(_dev.f64(a[None]), _dev.f64(b[None])))[0])

@@ -87,6 +87,57 @@ __global__ __launch_bounds__(256) void centroids_bf16x2_kernel(
   o[1] = a1;
 }
 
+// bf16, D % 8 == 0 (the decode/prefill path): each thread owns eight
+// adjacent dimensions — one 16-byte load per token row, so a half-warp reads
+// a whole 256-byte row of D = 128 — with 8 rows in flight (128 B per thread);
+// the per-dimension addition order is still token order (bit-exact).  The
+// eight fp64 results leave as four 16-byte stores.
+__global__ __launch_bounds__(256) void centroids_bf16x8_kernel(
+    const __nv_bfloat16* __restrict__ x, int64_t x_unit_stride, int D, Layout lay, int normalize,
+    double* __restrict__ out, int64_t out_unit_stride) {
+  const int u = blockIdx.y;
+  const int D8 = D / 8;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = (int)(idx / D8);
+  const int d = 8 * (int)(idx - (int64_t)c * D8);
+  if (c >= lay.num_chunks(u)) return;
+  int lo, hi;
+  lay.chunk(u, c, lo, hi);
+  const uint4* src =
+      reinterpret_cast<const uint4*>(x + (int64_t)u * x_unit_stride + (int64_t)lo * D + d);
+  const int64_t rs = D8;  // row stride in 16-byte words
+  double a[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) a[j] = 0.0;
+  auto add_row = [&](const uint4 w) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __bfloat1622float2(h[j]);
+      a[2 * j] = __dadd_rn(a[2 * j], (double)f.x);
+      a[2 * j + 1] = __dadd_rn(a[2 * j + 1], (double)f.y);
+    }
+  };
+  int t = 0;
+  const int n = hi - lo;
+  for (; t + 8 <= n; t += 8) {
+    uint4 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = __ldg(src + (int64_t)(t + k) * rs);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) add_row(v[k]);
+  }
+  for (; t < n; ++t) add_row(__ldg(src + (int64_t)t * rs));
+  if (normalize) {
+    const double r = __dsqrt_rn((double)n);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] = __ddiv_rn(a[j], r);
+  }
+  double2* o = reinterpret_cast<double2*>(out + (int64_t)u * out_unit_stride + (int64_t)c * D + d);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) o[j] = make_double2(a[2 * j], a[2 * j + 1]);
+}
+
 }  // namespace dhsa
 
 using namespace dhsa;
@@ -110,7 +161,13 @@ extern "C" int dhsa_centroids(int dtype, const void* x, int64_t x_unit_stride, i
                                                    out_unit_stride);
       break;
     case DHSA_BF16:
-      if (D % 2 == 0 && ((uintptr_t)x & 3) == 0 && x_unit_stride % 2 == 0) {
+      if (D % 8 == 0 && ((uintptr_t)x & 15) == 0 && x_unit_stride % 8 == 0 &&
+          ((uintptr_t)out & 15) == 0 && out_unit_stride % 2 == 0) {
+        const int64_t w8 = (int64_t)layout.max_chunks * (D / 8);
+        dim3 g8((unsigned)((w8 + 255) / 256), (unsigned)U);
+        centroids_bf16x8_kernel<<<g8, 256, 0, s>>>((const __nv_bfloat16*)x, x_unit_stride, D, lay,
+                                                   normalize, out, out_unit_stride);
+      } else if (D % 2 == 0 && ((uintptr_t)x & 3) == 0 && x_unit_stride % 2 == 0) {
         const int64_t w2 = (int64_t)layout.max_chunks * (D / 2);
         dim3 g2((unsigned)((w2 + 255) / 256), (unsigned)U);
         centroids_bf16x2_kernel<<<g2, 256, 0, s>>>((const __nv_bfloat16*)x, x_unit_stride, D, lay,

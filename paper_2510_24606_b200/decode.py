@@ -354,6 +354,32 @@ class SparseDecoder:
         n = self.ntiles.cpu().numpy()
         return [t[i, : n[i]].copy() for i in range(self.items)]
 
+    def cost_counters(self, counters=None):
+        """The reference's cost accounting (masks.CostCounters, masks.py:38-52)
+        of every decode step since the last prefill, computed analytically
+        (the kernels count nothing): per step with g generated tokens, each
+        q head scores its unit's N_c prompt chunks + the generated chunk
+        (g >= 1) + the singleton (masks.py:166-167; group aggregation counts
+        one score per head, harness.py:300-301), and each selection row —
+        one per kv unit for "max"/"mean", one per q head for "none" — admits
+        min(budget, P + g + 1) pairs (masks.py:171-172).  Adds to
+        ``counters`` (a fresh CostCounters if None) and returns it."""
+        from .masks import CostCounters
+
+        c = CostCounters() if counters is None else counters
+        P, n = self.max_prompt, self.steps
+        if n == 0:
+            return c
+        nc_heads = sum(self.chunk_counts) * self.G  # sum over q heads of N_c
+        # sum_{g=0}^{n-1} (N_c + [g >= 1] + 1) per q head
+        c.add_score_ops(nc_heads * n + self.U * self.G * ((n - 1) + n))
+        # sum_{g=0}^{n-1} min(budget, P + g + 1) per selection row
+        lo, hi = P + 1, P + n  # row sizes before the budget clamp
+        full = max(0, min(hi, self.budget - 1) - lo + 1) if lo < self.budget else 0
+        grow = (lo + lo + full - 1) * full // 2 if full else 0
+        c.add_attended(self.items * (grow + (n - full) * self.budget))
+        return c
+
     def bytes_per_step(self) -> dict:
         """Algorithmic (unique) HBM bytes of one step, the roofline numerator
         (fp64 centroids + selected K/V rows + q/o)."""

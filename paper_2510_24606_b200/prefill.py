@@ -279,6 +279,28 @@ class SparsePrefill:
             out.extend(range(start, start + lim))
         return np.sort(np.array(out, dtype=np.int64))
 
+    def cost_counters(self, counters=None):
+        """The reference's cost accounting (masks.CostCounters) of one call,
+        computed analytically: every q head scores its unit's N_c x N_c
+        chunk pairs (prefill_mask, masks.py:147-148; the head-aggregated
+        harness path counts one matrix per head, harness.py:300-301), and
+        each selection row's mask admits sum_i min(budget, i + 1) pairs
+        (mask_from_chunk_scores, masks.py:138-139).  Adds to ``counters``
+        (a fresh CostCounters if None) and returns it."""
+        from .masks import CostCounters
+
+        c = CostCounters() if counters is None else counters
+        if self.bounds_host is None:
+            ncs = [self.nc] * self.U
+        else:
+            ncs = [len(self.bounds_host[0 if len(self.bounds_host) == 1 else u]) - 1
+                   for u in range(self.U)]
+        c.add_score_ops(self.G * sum(n * n for n in ncs))
+        L, b = self.L, self.budget
+        m = min(L, b)
+        c.add_attended(self.S * (m * (m + 1) // 2 + (L - m) * b))
+        return c
+
     def flops(self) -> float:
         """Algorithmic flops: 4 * sum_i min(i+1, budget) * D per q head
         (QK^T and PV over the selected keys)."""

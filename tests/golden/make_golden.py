@@ -22,6 +22,16 @@ wire_*        DHSAMSK1 / DHSATEN1 / JSON files written by the reference's
               serialization.py (a prefill mask, a tensor) for byte-level parity
 nms.npz       nms_boundaries (chunking.py:57-89) on 300 random score vectors
               incl. forced ties, with random min_conf / window / max_chunks
+quality.npz   harness.compare (harness.py:346-401) on a planted corpus
+              (gen_planted, 3 sequences x 4 heads, L=256, d=32): per-(sequence,
+              method) recall / fidelity / score_ops / attended_pairs for dense,
+              static, dhsa_oracle and dhsa_predicted (init_predictor seed 5),
+              the masks of sequence 0, per-head attention_mass_recall /
+              output_fidelity, and causal_attention_probs of one small head
+quality_bf16.npz  the batched-engine shape: 2 planted sequences x 1 head,
+              L=1024, d=128, q/k/v rounded to bf16 values; per-row recall
+              fractions and sparse/dense cosines (harness.py:265-285) of the
+              static and dhsa_oracle masks at budget 129, sampled mask rows
 c1.npz        the C1 demo shape (L=4096, 8 heads, d=64, block 64, top-k 16,
               budget 1025): 3 decode steps per head, fp32-valued inputs,
               rows stored as (start, count) ranges + attention outputs
@@ -311,6 +321,104 @@ def gen_c1():
     np.savez_compressed(os.path.join(OUT, "c1.npz"), **blob)
 
 
+def _rows_blob(blob, key, rows):
+    iv, io = pack_rows(rows)
+    blob[key] = iv
+    blob[key + "_off"] = io
+
+
+def gen_quality():
+    from dhsa.core import causal_attention_probs, cosine_similarity
+    from dhsa.harness import PlantedCorpus, PlantedCorpusSpec, PlantedSequence, \
+        attention_mass_recall, compare, gen_planted, method_mask, output_fidelity
+    from dhsa.predictor import init_predictor
+
+    methods = ("dense", "static", "dhsa_oracle", "dhsa_predicted")
+    spec = PlantedCorpusSpec(num_sequences=3, length=256, dim=32, heads=4, seed=11)
+    corpus = gen_planted(spec)
+    pred = init_predictor(32, window=4, heads=8, hidden=64, seed=5)
+    kw = dict(budget=65, chunk_size=32, predictor=pred, min_conf=0.45, nms_window=8,
+              max_chunks=16)
+    rows, summary, _ = compare(corpus, methods=methods, **kw)
+    blob = {"budget": np.array(65), "chunk_size": np.array(32), "min_conf": np.array(0.45),
+            "nms_window": np.array(8), "max_chunks": np.array(16),
+            "pred_seed": np.array(5), "pred_hidden": np.array(64)}
+    for i, seq in enumerate(corpus.sequences):
+        blob[f"q_{i}"] = np.stack([h.queries for h in seq.heads])
+        blob[f"k_{i}"] = np.stack([h.keys for h in seq.heads])
+        blob[f"v_{i}"] = np.stack([h.values for h in seq.heads])
+        blob[f"bounds_{i}"] = np.array(seq.bounds)
+    blob["table"] = np.array([[r["sequence"], methods.index(r["method"]), r["score_ops"],
+                               r["attended_pairs"]] for r in rows], dtype=np.int64)
+    blob["recall"] = np.array([r["recall"] for r in rows])
+    blob["fidelity"] = np.array([r["fidelity"] for r in rows])
+    blob["summary"] = np.array([[summary[m]["mean_recall"], summary[m]["mean_fidelity"],
+                                 summary[m]["score_ops"], summary[m]["attended_pairs"],
+                                 summary[m]["total_ops"]] for m in methods])
+    seq0 = corpus.sequences[0]
+    for m in methods:
+        mask = method_mask(seq0, m, predictor=pred, **{k: v for k, v in kw.items()
+                                                       if k != "predictor"})
+        _rows_blob(blob, f"mask_{m}", mask.rows)
+    mask = method_mask(seq0, "dhsa_oracle", 65, chunk_size=32)
+    blob["head_recall"] = np.array([attention_mass_recall(causal_attention_probs(h), mask)
+                                    for h in seq0.heads])
+    blob["head_fidelity"] = np.array([output_fidelity(h, mask) for h in seq0.heads])
+    rng = np.random.default_rng(12)
+    small = TokenSequence(*(rng.standard_normal((40, 6)) for _ in range(3)))
+    blob["small_q"], blob["small_k"], blob["small_v"] = small.queries, small.keys, small.values
+    blob["small_probs"] = causal_attention_probs(small)
+    a, b = rng.standard_normal(9), rng.standard_normal(9)
+    blob["cos_ab"] = np.stack([a, b])
+    blob["cos"] = np.array([cosine_similarity(a, b), cosine_similarity(a, -a),
+                            cosine_similarity(np.zeros(9), b)])
+    np.savez_compressed(os.path.join(OUT, "quality.npz"), **blob)
+
+    # the batched engine's shape: one head per sequence (so the harness's
+    # head aggregation is the identity), d = 128, bf16-valued inputs
+    import torch
+
+    spec = PlantedCorpusSpec(num_sequences=2, length=1024, dim=128, heads=1, num_segments=8,
+                             seed=12)
+    corpus = gen_planted(spec)
+
+    def bf16(x):
+        return torch.from_numpy(np.asarray(x)).to(torch.bfloat16).to(torch.float64).numpy()
+
+    seqs = []
+    for seq in corpus.sequences:
+        h = seq.heads[0]
+        seqs.append(PlantedSequence(seq.attention, seq.bounds,
+                                    (TokenSequence(bf16(h.queries), bf16(h.keys),
+                                                   bf16(h.values)),)))
+    corpus = PlantedCorpus(spec, tuple(seqs))
+    budget = 129
+    blob = {"budget": np.array(budget)}
+    sample = np.arange(0, 1024, 37)
+    blob["sample"] = sample
+    for i, seq in enumerate(corpus.sequences):
+        h = seq.heads[0]
+        blob[f"q_{i}"], blob[f"k_{i}"], blob[f"v_{i}"] = h.queries, h.keys, h.values
+        blob[f"bounds_{i}"] = np.array(seq.bounds)
+        P = causal_attention_probs(h)
+        dense = dense_attention(h)
+        for m in ("static", "dhsa_oracle"):
+            mask = method_mask(seq, m, budget, chunk_size=64)
+            frac = np.array([P[r, idx].sum() / P[r, :r + 1].sum()
+                             for r, idx in enumerate(mask.rows)])
+            out = dense_attention(h, mask)
+            cos = np.array([cosine_similarity(out[r], dense[r]) for r in range(len(out))])
+            assert abs(frac.mean() - attention_mass_recall(P, mask)) < 1e-12
+            assert abs(cos.mean() - output_fidelity(h, mask, dense_out=dense)) < 1e-12
+            blob[f"recall_{m}_{i}"] = frac
+            blob[f"cos_{m}_{i}"] = cos
+            _rows_blob(blob, f"rows_{m}_{i}", [mask.rows[r] for r in sample])
+    rows, summary, _ = compare(corpus, budget, chunk_size=64, methods=("static", "dhsa_oracle"))
+    blob["summary"] = np.array([[summary[m]["mean_recall"], summary[m]["mean_fidelity"]]
+                                for m in ("static", "dhsa_oracle")])
+    np.savez_compressed(os.path.join(OUT, "quality_bf16.npz"), **blob)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:  # regenerate selected fixtures only, e.g. `nms`
         for name in sys.argv[1:]:
@@ -325,4 +433,5 @@ if __name__ == "__main__":
     gen_nms()
     gen_wire()
     gen_predictor()
+    gen_quality()
     print("golden fixtures written to", OUT)

@@ -182,3 +182,39 @@ def test_softmax_row_reference_cases(rng):
     for bad in (np.zeros(0), np.zeros((2, 2)), np.array([1.0, np.inf])):
         with pytest.raises(ValueError):
             P.softmax_row(bad)
+
+
+@pytest.mark.parametrize("D", [128, 64, 6, 5])
+def test_centroids_bf16_kernels_bitwise(D):
+    """K1 over bf16 inputs (the decode / prefill cache dtype) through every
+    load width — 16-byte rows (D % 8 == 0), bf16x2 (D even), scalar — with
+    static and ragged explicit chunks, bitwise equal to the sequential fp64
+    sums of chunk_repr.py:29-68 (oracle centroids pinned to the reference)."""
+    import torch
+
+    from paper_2510_24606_b200 import _lib
+
+    rng = np.random.default_rng(D)
+    U, L = 3, 700
+    x = torch.from_numpy(rng.standard_normal((U, L, D), dtype=np.float32) * 7).bfloat16().cuda()
+    xh = x.double().cpu().numpy()
+    ragged = [0, 1, 9, 64, 65, 200, 333, 334, 600, 700]
+    for bounds in (None, ragged):
+        plen = torch.full((U,), L, dtype=torch.int32, device="cuda")
+        if bounds is None:
+            nc = (L + 63) // 64
+            lay = _lib.layout(plen=plen, block=64, max_chunks=nc)
+            bl = O.static_grid(L, 64)
+        else:
+            nc = len(bounds) - 1
+            kb = torch.tensor([bounds] * U, dtype=torch.int32, device="cuda")
+            ncs = torch.full((U,), nc, dtype=torch.int32, device="cuda")
+            lay = _lib.layout(bounds=kb, bounds_stride=nc + 1, nchunks=ncs, plen=plen,
+                              max_chunks=nc)
+            bl = bounds
+        out = torch.zeros(U, nc, D, dtype=torch.float64, device="cuda")
+        _lib.call("dhsa_centroids", _lib.BF16, _lib.ptr(x), L * D, D, U, lay, 1, _lib.ptr(out),
+                  nc * D, _lib.stream_handle())
+        got = out.cpu().numpy()
+        for u in range(U):
+            assert np.array_equal(got[u], O.centroids(xh[u], bl)), (D, u, bounds)

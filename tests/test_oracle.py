@@ -100,3 +100,26 @@ def test_walk_equals_token_topk_random(rng):
         a = O.token_topk(tok, row, budget)
         b = O.ranges_to_indices(O.walk_ranges(s, bounds, row, budget), row)
         assert np.array_equal(a, b)
+
+
+def test_mask_quality_oracle_pinned_to_reference_harness():
+    """oracle.mask_quality (the checker of the GPU mask-quality metrics) vs
+    the reference harness's own per-row attention_mass_recall fractions and
+    output_fidelity cosines (harness.py:265-285, quality_bf16.npz from
+    make_golden.gen_quality), with the oracle's own prefill rows."""
+    import golden_io as G
+
+    z = G.load("quality_bf16.npz")
+    budget = int(z["budget"])
+    for i in range(2):
+        q, k, v = z[f"q_{i}"], z[f"k_{i}"], z[f"v_{i}"]
+        L = q.shape[0]
+        for m in ("static", "dhsa_oracle"):
+            bounds = O.static_grid(L, 64) if m == "static" else [int(x) for x in z[f"bounds_{i}"]]
+            rows = O.prefill_rows(q, k, bounds, budget)
+            want = G.unpack_rows(z[f"rows_{m}_{i}"], z[f"rows_{m}_{i}_off"])
+            for r, w in zip(z["sample"], want):
+                assert np.array_equal(rows[r], w), (i, m, r)
+            rec, cos = O.mask_quality(q, k, v, rows)
+            np.testing.assert_allclose(rec, z[f"recall_{m}_{i}"], rtol=0, atol=1e-12)
+            np.testing.assert_allclose(cos, z[f"cos_{m}_{i}"], rtol=0, atol=1e-12)
