@@ -244,6 +244,87 @@ def cpu_baseline(name, units_sample=None, steps=2, workers=None, shape=None):
     }
 
 
+def _c5_ref_head(args):
+    """One head of the C5 prefill through the reference at length L
+    (BASELINE.md section 2): prefill_mask (masks.py:143-150, timed whole) and
+    the dense_attention row body (core.py:113-118) on `rows_sample` rows
+    spread over the sequence, scaled to all L rows.  Returns (mask_s,
+    attn_s)."""
+    L, D, budget, rows_sample, seed = args
+    use_ref = reference_available()
+    rng = np.random.default_rng(seed)
+    import torch
+
+    q, k, v = (torch.from_numpy(rng.standard_normal((L, D), dtype=np.float32)).bfloat16()
+               .double().numpy() for _ in range(3))
+    if use_ref:
+        if REF_DIR not in sys.path:
+            sys.path.insert(0, REF_DIR)
+        from dhsa import TokenSequence, prefill_mask, softmax_row, static_boundaries
+
+        seq = TokenSequence(q, k, v)
+        t0 = time.perf_counter()
+        rows = prefill_mask(seq, static_boundaries(L, 64), budget).rows
+        mask_s = time.perf_counter() - t0
+    else:
+        from oracle import dhsa_oracle as O
+
+        t0 = time.perf_counter()
+        rows = O.prefill_rows(q, k, O.static_grid(L, 64), budget)
+        mask_s = time.perf_counter() - t0
+        softmax_row = None
+    inv = 1.0 / np.sqrt(D)
+    pick = np.linspace(0, L - 1, rows_sample).astype(np.int64)
+    t0 = time.perf_counter()
+    for i in pick:
+        idx = np.unique(np.asarray(rows[i], dtype=np.intp))  # _mask_rows, core.py:80-95
+        sc = np.einsum("jd,d->j", k[idx], q[i]) * inv
+        if softmax_row is not None:
+            softmax_row(sc) @ v[idx]
+        else:
+            e = np.exp(sc - sc.max())
+            (e / e.sum()) @ v[idx]
+    attn_s = (time.perf_counter() - t0) / rows_sample * L
+    return mask_s, attn_s
+
+
+def cpu_baseline_c5(Hq=32, Hkv=8, D=128, L=32768, top_k=64):
+    """C5 on the host: one head at 8K and at 16K
+    tokens, in two concurrent single-threaded processes; the mask time is
+    extrapolated to 32K with the measured 8K -> 16K growth exponent, the
+    attention linearly (rows past the budget each cost `budget` keys).  The
+    32K sequence = Hkv group-shared masks + Hq attention heads, spread over
+    the host cores (independent heads)."""
+    import multiprocessing as mp
+
+    budget = top_k * 64 + 1
+    lens = (8192, 16384)
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(2) as pool:
+        res = pool.map(_c5_ref_head, [(n, D, budget, 512, 5 + i) for i, n in enumerate(lens)])
+    wall = time.perf_counter() - t0
+    (m8, a8), (m16, a16) = res
+    alpha = float(np.log2(m16 / m8))
+    mask32 = m16 * (L / lens[1]) ** alpha
+    attn32 = a16 * L / lens[1]
+    cores = os.cpu_count() or 1
+    serial = Hkv * mask32 + Hq * attn32
+    # heads are independent: ceil(tasks / cores) rounds of the longest task
+    rounds = -(-(Hkv + Hq) // cores)
+    par = max(serial / cores, rounds * max(mask32, attn32)) if cores < Hkv + Hq else \
+        max(mask32, attn32)
+    kind = "reference" if reference_available() else "port"
+    return {"value": par * 1e3, "unit": "ms", "cores": min(cores, Hkv + Hq), "kind": kind,
+            "single_core_ms": serial * 1e3,
+            "sample": (f"top_k {top_k} (budget {budget}), one head at 8K and 16K tokens "
+                       f"({'baseline/_ref dhsa.prefill_mask + softmax_row row body' if kind == 'reference' else 'oracle prefill_rows + row body'}): "
+                       f"mask {m8:.2f} s / {m16:.2f} s (growth exponent {alpha:.2f}), "
+                       f"attention {a8:.2f} s / {a16:.2f} s (512 sampled rows each, scaled); "
+                       f"extrapolated to 32K: mask {mask32:.1f} s per kv group, attention "
+                       f"{attn32:.1f} s per q head; {Hkv} masks + {Hq} heads = {serial:.0f} s on "
+                       f"one core, spread over {min(cores, Hkv + Hq)} cores; wall {wall:.1f} s")}
+
+
 # ------------------------------------------------------------- GPU bench --
 def dist_setup():
     import torch
@@ -766,6 +847,8 @@ def run_gpu_c5(args):
         "sweep": sweep, "mask_quality": quality, "dynamic_chunks": dynamic,
         "gpu_launches": 5 * S, "clocks": clk.summary(),
     }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        result["cpu_baseline"] = cpu_baseline_c5(Hq, Hkv, D, L, head["top_k"])
     if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:

@@ -45,4 +45,12 @@ timeout 900 ncu --set full --clock-control none --import-source on \
   -k regex:"gemm_f64|window_attn|fuse_kernel|mlp_head" -s 6 -c 6 \
   -o $out/prof_pred -f python bench.py --config C5 --c5-topk 64 --steps 1 --warmup 1 --no-quality \
   > $out/ncu_pred.log 2>&1
+# the .ncu-rep files are too large to travel back: export the details and raw
+# pages as CSV next to them and drop the reports
+for r in $out/prof_*.ncu-rep; do
+  b=${r%.ncu-rep}
+  ncu -i $r --page details --csv > $b.details.csv 2>/dev/null
+  ncu -i $r --page raw --csv > $b.raw.csv 2>/dev/null
+  rm -f $r
+done
 ls -la $out
