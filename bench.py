@@ -680,13 +680,17 @@ def run_gpu_c4(args):
         "config": {"workload": f"C4 split-KV decode: 1 sequence, context={L}, Hq={Hq}, Hkv={Hkv}, "
                                f"d={D}, block={blk}, top_k={K}, {world} sequence shard(s)",
                    "context": L, "shards": world, "graphs": graphed,
+                   "path": ("one shard: the plain decode step (select -> attention, no exchange)"
+                            if sh.direct else "split-KV: candidates, all-gather, global walk, "
+                            "attention records, all-gather, merge"),
                    "exchange_bytes_per_rank": sh.bytes_per_step()["exchange"]},
         "step_roofline": {"bytes_per_step_per_gpu": sketch_b + kv_b,
                           "roofline_us": (sketch_b + kv_b) / (peak * 1e9) * 1e6,
                           "peak": peak, "peak_source": peak_src,
                           "frac": (sketch_b + kv_b) / (ms_step * 1e-3) / 1e9 / peak,
-                          "note": "latency-bound: 5 kernels + 2 all-gathers per step"},
-        "gpu_launches": SplitKVShard.kernels_per_step * n_steps, "clocks": clk.summary(),
+                          "note": "latency-bound" + ("" if sh.direct else
+                                                     ": 5 kernels + 2 all-gathers per step")},
+        "gpu_launches": sh.kernels_per_step * n_steps, "clocks": clk.summary(),
     }
     if graph_err:
         result["config"]["graph_note"] = graph_err
@@ -696,6 +700,77 @@ def run_gpu_c4(args):
         import torch.distributed as dist
 
         dist.destroy_process_group()
+
+
+def run_gpu_c4_proxy(args):
+    """C4 on N GPUs, proxied on one: the N shards of the 1M-token sequence as
+    a SplitKVGroup in one process (every kernel of the N-GPU step, the two
+    exchanges as device copies), one CUDA graph per step.  The shards'
+    kernels run one after another here, so the step time / N is one rank's
+    kernel time on N GPUs; the two all-gathers of the real run (NCCL over
+    NVLink, ~30 KB per rank each) are not included."""
+    import torch
+
+    from paper_2510_24606_b200.splitkv import SplitKVGroup
+
+    dist_setup()
+    B, Hq, Hkv, D, L, blk, K, dtn = CONFIGS["C4"]
+    N = args.rank_proxy
+    W, S = args.warmup, args.steps
+    nslot = W + S
+    grp = SplitKVGroup(B, Hq, Hkv, D, L, N, block=blk, top_k=K, max_new=nslot + 8)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(4321)
+    for sh in grp.shards:
+        d = sh.dec
+        for t in (d.k_cache, d.v_cache):
+            t[:, :, :sh.local_len].normal_(generator=gen)
+        d.prefill(d.k_cache, d.v_cache, prompt_len=sh.local_len)
+    qs = torch.randn(nslot, B, Hq, D, device="cuda", generator=gen).bfloat16()
+    ks = torch.randn(nslot, B, Hkv, D, device="cuda", generator=gen).bfloat16()
+    vs = torch.randn(nslot, B, Hkv, D, device="cuda", generator=gen).bfloat16()
+    out = torch.empty(B, Hq, D, dtype=torch.bfloat16, device="cuda")
+    grp.step(qs[0], ks[0], vs[0], out=out)
+    torch.cuda.synchronize()
+    stream = torch.cuda.Stream()
+    graphs = []
+    for i in range(1, nslot):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            grp.launch(qs[i], ks[i], vs[i], out, stream=stream)
+        graphs.append(g)
+    for i in range(1, W):
+        graphs[i - 1].replay()
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk, torch.cuda.stream(stream):
+        start.record(stream)
+        for i in range(W, nslot):
+            graphs[i - 1].replay()
+        end.record(stream)
+        torch.cuda.synchronize()
+    for sh in grp.shards:
+        sh.check_capacity()
+    ms_step = start.elapsed_time(end) / (nslot - W)
+    per_rank_us = ms_step * 1e3 / N
+    sh0 = grp.shards[0]
+    result = {
+        "metric": METRIC, "value": B / (per_rank_us * 1e-6), "unit": "tokens/s", "n_gpus": 1,
+        "steps": nslot - W, "warmup": W, "ms_per_step": per_rank_us / 1e3,
+        "us_per_step": per_rank_us, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic N(0,1) q/k/v, random-init KV cache",
+        "config": {"workload": f"C4 split-KV decode: 1 sequence, context={L}, Hq={Hq}, Hkv={Hkv}, "
+                               f"d={D}, block={blk}, top_k={K}, {N} sequence shards",
+                   "context": L, "shards": N, "graphs": True,
+                   "exchange_bytes_per_rank": sh0.bytes_per_step()["exchange"]},
+        "proxy": {"n_gpus": N, "group_us_per_step": ms_step * 1e3,
+                  "note": f"the {N} shards' kernels on one GPU, one after another, exchanges as "
+                          f"device copies; us_per_step = group step / {N} = one rank's kernel "
+                          f"time; the two NCCL all-gathers of the {N}-GPU run are not included"},
+        "gpu_launches": sum(s.kernels_per_step for s in grp.shards) * (nslot - W),
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(result), flush=True)
 
 
 def run_gpu_c5(args):
@@ -940,6 +1015,8 @@ def main():
     args.warmup_ref = args.warmup
     if args.impl == "reference":
         run_reference(args)
+    elif args.config == "C4" and args.rank_proxy > 1 and "WORLD_SIZE" not in os.environ:
+        run_gpu_c4_proxy(args)
     elif args.config == "C4":
         run_gpu_c4(args)
     elif args.config == "C5":

@@ -43,11 +43,13 @@ struct StreamArgs {
   __nv_bfloat16* out;
   float* rec_out;     // unnormalised records instead of out (split-KV shards)
   float* ws;          // [items][kStreamMaxSeg][GH][D+2]
-  int32_t* counters;  // [2]: pull counter, exits; zero at rest
+  int32_t* counters;  // [2 + 2 items]: pull counter, exits, per-item segment records
+                      // written, per-item merges done; zero at rest
   int32_t* ready;     // [items] or null (re-armed by the next step's first kernel)
   float scale_log2;
   int spin_ns;              // back-off of the ready-flag wait
   int l2_hint;              // evict-first L2 policy on the K/V stream
+  int merge_early;          // merges start per item (segment counters), not at grid end
   unsigned long long* dbg;  // DHSA_DEBUG_TIMING (common.cuh)
 };
 
@@ -244,6 +246,14 @@ __global__ __launch_bounds__(192, 2) void attn_stream_kernel(const __grid_consta
                            : slots + (j * GH + h) * REC;
         store_row<D>(a, item, h, d, mstar, lsum, acc, rec);
       }
+      if (!whole && a.merge_early) {
+        // the segment's record is complete: count it for the item's merge,
+        // which starts as soon as all of its records exist (not when the grid
+        // ends); every lane's stores are fenced before lane 0's count
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(a.counters + 2 + item, 1);
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&epi_empty);  // red[] may be overwritten now
     }
@@ -315,7 +325,11 @@ __global__ __launch_bounds__(192, 2) void attn_stream_kernel(const __grid_consta
 
 // Items processed by more than one segment: merge the slot records in slot
 // order (deterministic).  One CTA per (item, head), one thread per dimension;
-// launched programmatically after the attention grid (griddepcontrol.wait).
+// launched programmatically with the attention grid: a CTA starts merging as
+// soon as its item's segment records are all written (per-item counter,
+// acquire), and waits for the attention grid's completion (griddepcontrol.
+// wait) only at its end, so the merge overlaps the attention's tail and the
+// stream order of the following kernels is unchanged.
 template <int D>
 __global__ __launch_bounds__(D) void stream_merge_kernel(StreamArgs a) {
   constexpr int REC = D + 2;
@@ -329,13 +343,28 @@ __global__ __launch_bounds__(D) void stream_merge_kernel(StreamArgs a) {
     __syncthreads();
   }
   const int nt = __ldcg(a.ntiles + item);
-  pdl_wait();
-  if (a.dbg && threadIdx.x == 0) atomicMin(a.dbg + kDbgAttn + 8192, gtimer());
   int lo, hi;
   int S, nseg;
   seg_shape(a, item, S, nseg);
   seg_range(0, S, nseg, nt, lo, hi);
-  if (hi - lo == nt) return;  // one segment: written directly by the attention
+  if (hi - lo == nt) {  // one segment: written directly by the attention
+    pdl_wait();
+    return;
+  }
+  int nrec = 0;  // segments holding tiles = records the attention writes
+  for (int sg = 0; sg < nseg; ++sg) {
+    seg_range(sg, S, nseg, nt, lo, hi);
+    nrec += lo < hi ? 1 : 0;
+  }
+  int32_t* seg_done = a.counters + 2 + item;
+  int32_t* merged = a.counters + 2 + a.items + item;
+  if (a.merge_early) {
+    if (threadIdx.x == 0) spin_geq(seg_done, nrec);
+    __syncthreads();
+  } else {
+    pdl_wait();
+  }
+  if (a.dbg && threadIdx.x == 0) atomicMin(a.dbg + kDbgAttn + 8192, gtimer());
   const float* slots = a.ws + (int64_t)item * kStreamMaxSeg * GH * REC + h * REC;
   float mv[kStreamMaxSeg], lv[kStreamMaxSeg], av[kStreamMaxSeg];
 #pragma unroll
@@ -366,6 +395,15 @@ __global__ __launch_bounds__(D) void stream_merge_kernel(StreamArgs a) {
   store_row<D>(a, item, h, d, mstar, lsum, acc,
                a.rec_out ? a.rec_out + ((int64_t)item * GH + h) * REC : nullptr);
   if (a.dbg && threadIdx.x == 0) atomicMax(a.dbg + kDbgAttn + 8193, gtimer());
+  // the last of the item's GH merge CTAs re-arms its counters (every CTA has
+  // passed its wait on seg_done by then)
+  if (a.merge_early) {
+    if (threadIdx.x == 0 && atomicAdd(merged, 1) == GH - 1) {
+      *seg_done = 0;
+      *merged = 0;
+    }
+    pdl_wait();
+  }
 }
 
 template <int D, int STAGES>
@@ -438,7 +476,7 @@ extern "C" int64_t dhsa_attn_stream_workspace_size(int items, int GH, int D) {
   return (int64_t)items * kStreamMaxSeg * GH * (D + 2) * 4;
 }
 
-extern "C" int dhsa_attn_stream_counters(int items) { return items + 2; }  // (>= 2 used)
+extern "C" int dhsa_attn_stream_counters(int items) { return 2 * items + 2; }
 
 extern "C" int dhsa_attn_stream(const void* q, const void* k_cache, const void* v_cache,
                                 int64_t cache_unit_stride, int64_t cache_rows, int items,
@@ -494,6 +532,8 @@ extern "C" int dhsa_attn_stream(const void* q, const void* k_cache, const void* 
   a.l2_hint = 1;
   if (const char* e = getenv("DHSA_L2_HINT")) a.l2_hint = atoi(e);
   if (const char* e = getenv("DHSA_SPIN_NS")) a.spin_ns = atoi(e);
+  a.merge_early = 0;
+  if (const char* e = getenv("DHSA_MERGE_EARLY")) a.merge_early = atoi(e);
   cudaStream_t s = (cudaStream_t)stream;
   int stages = 3;
   if (const char* e = getenv("DHSA_STREAM_STAGES")) stages = atoi(e);

@@ -219,6 +219,9 @@ __device__ __forceinline__ int ld_acquire(const int32_t* p) {
 __device__ __forceinline__ void st_release(int32_t* p, int v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void st_relaxed(int32_t* p, int v) {
+  asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 // Release-add: prior writes of this thread (and, via a preceding warp/CTA
 // barrier, of its peers) become visible before the increment.
 __device__ __forceinline__ void red_add_release(int32_t* p, int v) {

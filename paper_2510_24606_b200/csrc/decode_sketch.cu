@@ -615,41 +615,72 @@ __global__ void sketch_absmax_kernel(const double* __restrict__ cent, int64_t c_
   }
 }
 
-// pass 2: scale, round to fp16, measure ||c''|| and ||c'' - c 2^-k|| per chunk
+// pass 2: scale, round to fp16, measure ||c''|| and ||c'' - c 2^-k|| per chunk.
+// A warp per chunk (lane l owns dims 4l .. 4l+3 of every 128: two 16-byte
+// fp64 loads, one 8-byte fp16 store), kSketchChunksPerCta chunks per CTA; the
+// per-chunk bounds are reduced in the CTA first, so each CTA issues ONE pair
+// of atomics on its unit's sinfo (one pair per chunk serialised on the same
+// address made the r1 kernel atomic-bound: 0.15 of HBM at C3).
+constexpr int kSketchChunksPerCta = 64;
+
 __global__ __launch_bounds__(256) void sketch_build_kernel(const double* __restrict__ cent,
                                                            int64_t c_stride, int D, Layout lay,
                                                            __half* __restrict__ sk,
                                                            int64_t sk_stride,
                                                            float* __restrict__ sinfo) {
+  __shared__ float s_fn[8], s_fe[8];
   const int u = blockIdx.y;
-  const int lane = threadIdx.x & 31;
-  const int c = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (c >= lay.num_chunks(u)) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nc = lay.num_chunks(u);
+  const int c0 = blockIdx.x * kSketchChunksPerCta;
+  if (c0 >= nc) return;  // uniform over the CTA
   const float amax = sinfo[4 * u + 3];
   int k = 0;
   if (amax > 0.f && isfinite(amax)) k = ilogb((double)amax) + 1 - 14;  // max|c| 2^-k < 2^14
   const double sc = ldexp(1.0, -k);
-  const double* src = cent + (int64_t)u * c_stride + (int64_t)c * D;
-  __half* dst = sk + (int64_t)u * sk_stride + (int64_t)c * D;
-  double nrm = 0.0, err = 0.0;
-  bool finite = isfinite(amax);
-  for (int d = lane; d < D; d += 32) {
-    const double v = src[d] * sc;  // exact (power of two)
-    const __half h = __double2half(v);
-    dst[d] = h;
-    const double hv = (double)__half2float(h);
-    finite = finite && isfinite(hv);
-    nrm = fma(hv, hv, nrm);
-    err = fma(hv - v, hv - v, err);
-  }
-  nrm = warp_sum(nrm);
-  err = warp_sum(err);
-  finite = __all_sync(0xffffffffu, finite);
-  if (lane == 0) {
-    if (blockIdx.x == 0 && c == 0) sinfo[4 * u + 0] = (float)k;
+  const bool afin = isfinite(amax);
+  float wfn = 0.f, wfe = 0.f;
+  for (int c = c0 + warp; c < min(c0 + kSketchChunksPerCta, nc); c += 8) {
+    const double* src = cent + (int64_t)u * c_stride + (int64_t)c * D;
+    __half* dst = sk + (int64_t)u * sk_stride + (int64_t)c * D;
+    double nrm = 0.0, err = 0.0;
+    bool finite = afin;
+    for (int d = 4 * lane; d < D; d += 128) {
+      const double2 a = __ldcs(reinterpret_cast<const double2*>(src + d));
+      const double2 b = __ldcs(reinterpret_cast<const double2*>(src + d + 2));
+      const double v[4] = {a.x * sc, a.y * sc, b.x * sc, b.y * sc};  // exact (power of two)
+      __align__(8) __half h[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        h[j] = __double2half(v[j]);
+        const double hv = (double)__half2float(h[j]);
+        finite = finite && isfinite(hv);
+        nrm = fma(hv, hv, nrm);
+        err = fma(hv - v[j], hv - v[j], err);
+      }
+      *reinterpret_cast<uint2*>(dst + d) = *reinterpret_cast<const uint2*>(h);
+    }
+    nrm = warp_sum(nrm);
+    err = warp_sum(err);
+    finite = __all_sync(0xffffffffu, finite);
     // a non-finite sketch makes E infinite: every chunk is then re-scored
     const float fn = finite ? __double2float_ru(sqrt(nrm) * (1.0 + 1e-9)) : INFINITY;
     const float fe = finite ? __double2float_ru(sqrt(err) * (1.0 + 1e-9)) : INFINITY;
+    wfn = fmaxf(wfn, fn);
+    wfe = fmaxf(wfe, fe);
+  }
+  if (lane == 0) {
+    s_fn[warp] = wfn;
+    s_fe[warp] = wfe;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float fn = s_fn[0], fe = s_fe[0];
+    for (int w = 1; w < 8; ++w) {
+      fn = fmaxf(fn, s_fn[w]);
+      fe = fmaxf(fe, s_fe[w]);
+    }
+    if (blockIdx.x == 0) sinfo[4 * u + 0] = (float)k;
     atomicMax(reinterpret_cast<unsigned int*>(sinfo + 4 * u + 1), __float_as_uint(fn));
     atomicMax(reinterpret_cast<unsigned int*>(sinfo + 4 * u + 2), __float_as_uint(fe));
   }
@@ -753,13 +784,17 @@ extern "C" int dhsa_sketch_build(const double* centroids, int64_t c_unit_stride,
                                  float* sinfo, dhsa_stream_t stream) {
   DHSA_REQUIRE(centroids && sketch && sinfo && D >= 1 && U >= 1, "dhsa_sketch_build: bad arguments");
   DHSA_REQUIRE(valid_layout(layout) && layout.max_chunks >= 1, "dhsa_sketch_build: bad layout");
+  DHSA_REQUIRE(D % 4 == 0 && c_unit_stride % 2 == 0 && sk_unit_stride % 4 == 0 &&
+                   ((uintptr_t)centroids & 15) == 0 && ((uintptr_t)sketch & 7) == 0,
+               "dhsa_sketch_build: D % 4 == 0 and aligned centroid / sketch rows required");
   cudaStream_t s = (cudaStream_t)stream;
   cudaMemsetAsync(sinfo, 0, sizeof(float) * 4 * U, s);
   Layout lay(layout);
   const int64_t work = (int64_t)layout.max_chunks * D;
   dim3 g1((unsigned)((work + 255) / 256 < 64 ? (work + 255) / 256 : 64), (unsigned)U);
   sketch_absmax_kernel<<<g1, 256, 0, s>>>(centroids, c_unit_stride, D, lay, sinfo);
-  dim3 g2((unsigned)((layout.max_chunks + 7) / 8), (unsigned)U);
+  dim3 g2((unsigned)((layout.max_chunks + kSketchChunksPerCta - 1) / kSketchChunksPerCta),
+          (unsigned)U);
   sketch_build_kernel<<<g2, 256, 0, s>>>(centroids, c_unit_stride, D, lay, (__half*)sketch,
                                          sk_unit_stride, sinfo);
   return check_launch("dhsa_sketch_build");
@@ -852,6 +887,7 @@ static int decode_step_impl(
   if (const char* e = getenv("DHSA_L2_HINT")) a.l2_hint = atoi(e);
   a.reps = 1;
   if (const char* e = getenv("DHSA_SELECT_REPS")) a.reps = atoi(e) > 0 ? atoi(e) : 1;
+  if (const char* e = getenv("DHSA_RELAXED_FLAGS")) a.relaxed = atoi(e);
   const int64_t need = select_scratch_per_unit(layout.max_chunks);
   size_t smem = 0;
   if (scratch) {

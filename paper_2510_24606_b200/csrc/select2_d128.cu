@@ -10,12 +10,13 @@ template <int D, int G, int AGG>
 int launch_select2(const SketchArgs& a, int U, cudaStream_t s, int* rc) {
   // the massive-tie fallback keeps its keys in global scratch; split-KV
   // candidate mode and longer units use the generic select
-  if (!a.gscratch || a.split || a.n_max > kS3MaxChunks) return 0;
+  if (!a.gscratch || a.split || a.n_max > kS3WideMaxChunks) return 0;
   if (const char* e = getenv("DHSA_SELECT2"))
     if (atoi(e) == 0) return 0;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)U);
-  cfg.blockDim = dim3(kS3Threads);
+  const bool wide = a.n_max > kS3MaxChunks;
+  cfg.blockDim = dim3(wide ? kS3WideThreads : kS3Threads);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -23,7 +24,9 @@ int launch_select2(const SketchArgs& a, int U, cudaStream_t s, int* rc) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, sketch_select3_kernel<D, G, AGG>, a);
+  cudaError_t e =
+      wide ? cudaLaunchKernelEx(&cfg, sketch_select3_kernel<D, G, AGG, kS3WideThreads, kS3WidePer>, a)
+           : cudaLaunchKernelEx(&cfg, sketch_select3_kernel<D, G, AGG, kS3Threads, kS3Per>, a);
   if (e != cudaSuccess) {
     set_error("dhsa_decode_step_bf16(select): %s", cudaGetErrorString(e));
     *rc = DHSA_ECUDA;

@@ -126,8 +126,12 @@ class SplitKVShard:
 
     def __init__(self, batch, q_heads, kv_heads, head_dim, prompt_len, *, rank, world,
                  block=64, top_k=64, budget=None, agg="max", max_new=1024, tile=64,
-                 splits=None, device=None, attn_mode=None, bounds=None):
+                 splits=None, device=None, attn_mode=None, bounds=None, direct=True):
         self.rank, self.world = int(rank), int(world)
+        # one shard holds the whole sequence: its step is the plain batched
+        # decode (select -> attention, no candidate records, exchange or
+        # record merge); direct=False keeps the split kernels (tests)
+        self.direct = bool(direct) and self.world == 1
         self.block = int(block)
         self.total_prompt = int(prompt_len)
         self.local_bounds = None
@@ -236,6 +240,9 @@ class SplitKVShard:
     def launch(self, q, k_new, v_new, comm, out, stream=None):
         """Enqueue one step on the current (or given) stream: 4 kernels + 2
         all-gathers; graph-capturable when the collective is."""
+        if self.direct:
+            self.dec.launch(q, k_new, v_new, out, stream=stream)
+            return
         self.candidates(q, k_new, v_new, stream)
         if comm.world == 1:  # one shard: the gathered rows are this shard's own
             self.select(self.cand, stream=stream)
@@ -248,7 +255,12 @@ class SplitKVShard:
         comm.all_gather(self.rec_all, self.rec)
         self.merge(out, stream=stream)
 
-    kernels_per_step = 5  # sketch stream, candidate select, global walk, attention, merge
+    @property
+    def kernels_per_step(self) -> int:
+        """sketch stream, candidate select, global walk, attention, merge (+
+        the segment merge); one shard: the plain decode step's kernels."""
+        return self.dec.kernels_per_step if self.direct else 5 + (
+            self.dec.kernels_per_step - 3)
 
     def selection(self):
         """This shard's tiles (local token ranges) of the last step."""
@@ -299,6 +311,23 @@ class SplitKVGroup:
         for s in sh:
             s.dec.steps += 1
         return out
+
+    def launch(self, q, k_new, v_new, out, stream=None):
+        """One step enqueued on the current stream without host allocation
+        (graph-capturable): the exchanges are device copies into shard 0's
+        gather buffers, which every shard's global walk reads."""
+        sh = self.shards
+        g, n = sh[0].gathered, sh[0].cand.numel()
+        for r, s in enumerate(sh):
+            s.candidates(q, k_new, v_new, stream)
+            g[r * n:(r + 1) * n].copy_(s.cand)
+        for s in sh:
+            s.select(g, stream=stream)
+            s.attend(q, stream)
+        ra, m = sh[0].rec_all, sh[0].rec.numel()
+        for r, s in enumerate(sh):
+            ra[r * m:(r + 1) * m].copy_(s.rec)
+        sh[0].merge(out, ra, stream=stream)
 
     def selection(self):
         """Per selection row: the union of every shard's tiles in GLOBAL token

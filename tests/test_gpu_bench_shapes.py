@@ -136,15 +136,20 @@ def _check_decode_step(sel, o, units, oracles, q_h, k_h, K, V, G, pos):
 
 # ------------------------------------------------------------------ C4 ----
 
-@pytest.mark.parametrize("P", [327680, 1048576])
-def test_c4_one_shard_wide_units(P):
-    """W=1 split-KV over 5,120 / 16,384 chunks per unit (the 1024-thread
-    select with global scratch) — the C4 bench's own path at 1M."""
+@pytest.mark.parametrize("P,direct", [(327680, True), (1048576, True), (327680, False),
+                                      (1048576, False)])
+def test_c4_one_shard_wide_units(P, direct):
+    """W=1 over 5,120 / 16,384 chunks per unit — the C4 bench's own path at
+    1M: direct = the plain decode step (the 1024-thread compact select,
+    17,408 chunks per CTA), else the split kernels (candidate-mode generic
+    1024-thread select with global scratch, global walk, record merge)."""
     from paper_2510_24606_b200.splitkv import LocalComm, SplitKVShard
 
     B, Hq, Hkv, D, steps = 1, 32, 8, 128, 3
     G = Hq // Hkv
-    sh = SplitKVShard(B, Hq, Hkv, D, P, rank=0, world=1, top_k=64, max_new=steps + 1)
+    sh = SplitKVShard(B, Hq, Hkv, D, P, rank=0, world=1, top_k=64, max_new=steps + 1,
+                      direct=direct)
+    assert sh.direct == direct
     g = _gen(P % 1000 + 1)
     d = sh.dec
     for t in (d.k_cache, d.v_cache):
