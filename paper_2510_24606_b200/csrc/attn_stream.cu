@@ -111,10 +111,12 @@ __global__ __launch_bounds__(192, 2) void attn_stream_kernel(const __grid_consta
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 4);
+      mbar_init(&empty_bar[s], 4 * 32);
     }
-    mbar_init(&epi_full, 4);
-    mbar_init(&epi_empty, 1);
+    // every lane that read (wrote) a shared buffer arrives itself: the
+    // hand-offs do not rest on __syncwarp cumulativity (racecheck-clean)
+    mbar_init(&epi_full, 4 * 32);
+    mbar_init(&epi_empty, 32);
     fence_barrier_init();
   }
   __syncthreads();
@@ -254,8 +256,7 @@ __global__ __launch_bounds__(192, 2) void attn_stream_kernel(const __grid_consta
         __syncwarp();
         if (lane == 0) atomicAdd(a.counters + 2 + item, 1);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&epi_empty);  // red[] may be overwritten now
+      mbar_arrive(&epi_empty);  // red[] may be overwritten now
     }
     if (a.dbg && lane == 0) a.dbg[kDbgAttn + 4 * c + 2] = gtimer();
     if (lane == 0) {  // the last CTA out re-arms the pull counter
@@ -290,13 +291,11 @@ __global__ __launch_bounds__(192, 2) void attn_stream_kernel(const __grid_consta
       if (a.dbg && first && threadIdx.x == 0) a.dbg[kDbgAttn + 4 * c + 1] = gtimer();
       first = false;
       T::update(smem_u32(smem + st * STAGE_BYTES), e.a, warp, lane, qa, a.scale_log2, m, l, o);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty_bar[st]);
+      mbar_arrive(&empty_bar[st]);
       ++ntile_done;
       continue;
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty_bar[st]);
+    mbar_arrive(&empty_bar[st]);
     // hand the segment (or the exit) to the epilogue warp once red[] is free
     if (nend > 0) mbar_wait(&epi_empty, (nend - 1) & 1);
     if (e.type == kEnd) {
@@ -311,8 +310,7 @@ __global__ __launch_bounds__(192, 2) void attn_stream_kernel(const __grid_consta
       T::warp_record(red, warp, lane, GH, m, l, o);
     }
     if (threadIdx.x == 0) epi_meta = e;
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&epi_full);
+    mbar_arrive(&epi_full);
     ++nend;
     if (e.type == kExit) break;
   }

@@ -689,6 +689,9 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_kernel(
       lsum += softmax_pack64(v, sl2, mref, pk);
       tmem_st32(tS + (j & 1) * 64, pk);  // P over the first 32 columns of its S buffer
       tmem_wait_st();
+      // observe every o_done phase (PV_{j-1}, long complete by now): no phase
+      // of the barrier passes unobserved, so a parity wait never aliases
+      if (j >= 1) mbar_wait(&o_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[j & 1]);
@@ -759,8 +762,11 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_persist_kernel(
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 4 * MT);
       mbar_init(&o_done[i], 1);
-      mbar_init(&plan_full[i], 1);
-      mbar_init(&plan_empty[i], 1 + 4 * MT);
+      // plan entries are shared-memory hand-offs: every lane that wrote
+      // (read) them arrives itself (racecheck-clean, no reliance on
+      // __syncwarp cumulativity)
+      mbar_init(&plan_full[i], 32);
+      mbar_init(&plan_empty[i], 1 + 4 * MT * 32);
     }
     mbar_init(&q_full, 1);
     mbar_init(&q_empty, 1);
@@ -796,13 +802,10 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_persist_kernel(
       int p = 0;
       if (lane == 0) p = atomicAdd(a.counters, 1);
       p = __shfl_sync(0xffffffffu, p, 0);
-      if (k >= 2 && lane == 0) mbar_wait(&plan_empty[b], ((k >> 1) - 1) & 1);
-      __syncwarp();
+      if (k >= 2) mbar_wait(&plan_empty[b], ((k >> 1) - 1) & 1);
       if (p >= total) {
-        if (lane == 0) {
-          s_meta[b] = make_int4(-1, 0, 0, 0);
-          mbar_arrive(&plan_full[b]);
-        }
+        if (lane == 0) s_meta[b] = make_int4(-1, 0, 0, 0);
+        mbar_arrive(&plan_full[b]);
         break;
       }
       int y, sr, hs, l = 0, qt = 0;
@@ -820,8 +823,8 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_persist_kernel(
         s_meta[b] = make_int4(p, np, l, sr * a.slices + hs);
         s_qt[b] = qt;
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&plan_full[b]);
+      __syncwarp();  // lane 0 reads the other lanes' entries below
+      mbar_arrive(&plan_full[b]);
       if (np <= 0) continue;  // capacity overflow: reported by the host
       if (lane == 0) {
         const int qh0 = (a.per_head ? sr : sr * a.G) + hs * a.heads_per_cta;
@@ -935,8 +938,7 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_persist_kernel(
       if (m.x < 0) break;
       const int np = m.y;
       if (np <= 0) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&plan_empty[b]);
+        mbar_arrive(&plan_empty[b]);
         continue;
       }
       const int l = m.z, sr = m.w / a.slices, hs = m.w - sr * a.slices;
@@ -996,6 +998,9 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_persist_kernel(
         lsum += softmax_pack64(v, sl2, mref, pk);
         tmem_st32(tS + (jj & 1) * 64, pk);
         tmem_wait_st();
+        // observe every o_done phase (PV_{jj-1}, long complete by now): no
+        // phase of the barrier passes unobserved, so a parity wait never aliases
+        if (jj >= 1) mbar_wait(&o_done[(jj - 1) & 1], ((jj - 1) >> 1) & 1);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[jj & 1]);
@@ -1025,10 +1030,8 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_persist_kernel(
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&o_free);         // the next plan's first PV may overwrite O
-        mbar_arrive(&plan_empty[b]);  // plan entries no longer read
-      }
+      if (lane == 0) mbar_arrive(&o_free);  // the next plan's first PV may overwrite O
+      mbar_arrive(&plan_empty[b]);           // plan entries no longer read (every lane)
       jg0 += np;
     }
   }
