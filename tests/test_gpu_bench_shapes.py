@@ -345,6 +345,58 @@ def test_certified_bound_near_ties(agg):
         assert np.array_equal(tiles_to_idx(sel[j]), want), j
 
 
+@pytest.mark.parametrize("pattern", ["gauss", "cancel", "spread"])
+def test_sketch_accumulation_error_model(pattern):
+    """The certified bound (decode_sketch.cu) models the
+    tensor-core score of a sketch row as |s'' - sum_d c''_d q_d| <= gamma *
+    sum_d |c''_d q_d| with gamma = 2^-14 + 1e-6 (fp16 x bf16 products exact
+    in fp32, fp32 accumulation inside mma.sync).  Checked on the hardware,
+    chunk by chunk and head by head, against the exact float64 dot products
+    of the very fp16 sketch rows and bf16 queries the kernel read: Gaussian
+    rows, rows whose products cancel exactly (every bit of the result is
+    accumulation error), and products spread over 2^-20 .. 2^0 with random
+    signs (alignment / truncation stress)."""
+    from paper_2510_24606_b200.decode import SparseDecoder
+
+    B, Hkv, G, D, nch = 1, 1, 4, 128, 512
+    P = 64 * nch
+    rng = np.random.default_rng({"gauss": 1, "cancel": 2, "spread": 3}[pattern])
+    if pattern == "gauss":
+        t = rng.standard_normal((nch, D))
+        qh = rng.standard_normal((G, D))
+    elif pattern == "cancel":
+        # half the dims +a, the other half -a permuted: the exact sum is 0
+        mag = 2.0 ** rng.integers(-10, 1, size=(nch, D // 2)) * rng.uniform(1, 2, size=(nch, D // 2))
+        t = np.concatenate([mag, -mag], axis=1)
+        qh = np.ones((G, D))
+        for j in range(nch):  # the same bf16 values, the cancelling halves interleaved
+            t[j] = t[j][rng.permutation(D)]
+    else:
+        t = (2.0 ** rng.integers(-20, 1, size=(nch, D)) * rng.uniform(1, 2, size=(nch, D))
+             * rng.choice([-1.0, 1.0], size=(nch, D)))
+        qh = (2.0 ** rng.integers(-6, 1, size=(G, D)) * rng.choice([-1.0, 1.0], size=(G, D)))
+    tb = torch.from_numpy(t).float().bfloat16()
+    k = tb.repeat_interleave(64, dim=0).view(B, Hkv, P, D).cuda()  # centroid = 8 t exactly
+    k = torch.cat([k, torch.zeros(B, Hkv, 1, D, dtype=torch.bfloat16, device="cuda")], dim=2)
+    v = torch.zeros_like(k)
+    q = torch.from_numpy(qh).float().bfloat16().view(B, Hkv * G, D).cuda()
+    dec = SparseDecoder(B, G, Hkv, D, P + 1, top_k=64, dtype=torch.bfloat16, agg="none")
+    dec.prefill(k[:, :, :P], v[:, :, :P])
+    dec.step(q, k[:, :, P].contiguous(), v[:, :, P].contiguous())
+    torch.cuda.synchronize()
+    sk = dec.sketch[0, 0, :nch].double().cpu().numpy()       # c'' (fp16, exact)
+    qd = q[0].double().cpu().numpy()                          # q (bf16, exact)
+    approx = dec.approx[:G, :nch].double().cpu().numpy()     # s'' per (head, chunk)
+    exact = qd @ sk.T
+    absum = np.abs(qd) @ np.abs(sk).T
+    gamma = 2.0 ** -14 + 1e-6
+    ratio = np.abs(approx - exact) / np.maximum(absum, 1e-300)
+    assert np.isfinite(approx).all()
+    print(f"{pattern}: max accumulation error / sum|p| = {ratio.max():.3e} (gamma {gamma:.3e})")
+    assert (np.abs(approx - exact) <= gamma * absum).all(), (
+        f"{pattern}: accumulation error {ratio.max():.3e} x sum|p| exceeds gamma {gamma:.3e}")
+
+
 # ------------------------------------------------------------------ C3 ----
 
 def test_c3_state_after_1500_steps():
