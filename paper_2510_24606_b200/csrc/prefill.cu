@@ -367,6 +367,7 @@ struct PrefillArgs {
   PrefillChunks ch;    // chunk layout (static grid or explicit bounds)
   const int2* qtiles;  // explicit bounds: [U][T] query tiles (chunk l, 64-row tile t),
   int T;               // heavy first, l = -1 pads; null with the static grid (T = nc)
+  unsigned long long* dbg;  // DHSA_DEBUG_TIMING: clock64 stamps of one CTA (prefill_timeline.py)
   // query tile y of unit u -> (chunk l, tile t); false for padding
   __device__ __forceinline__ bool tile(int u, int y, int& l, int& t) const {
     if (qtiles) {
@@ -544,6 +545,11 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_kernel(
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = s_tmem;
+  // debug timeline (one CTA: the heaviest query chunk of selection row 0)
+  unsigned long long* dbg =
+      (a.dbg && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) ? a.dbg : nullptr;
+#define PF_T(kind, j)                                                  \
+  if (dbg && lane == 0 && (j) < 256) dbg[(kind) * 256 + (j)] = clock64();
   const uint32_t sq = smem_u32(smem + SM::q_off);
   const uint32_t skv = smem_u32(smem + SM::kv_off);
 
@@ -581,7 +587,9 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_kernel(
       mbar_wait(&q_full, 0);
       auto issue_s = [&](int j) {
         const int st = j % NST;
+        PF_T(0, j);
         mbar_wait(&kv_full[st], (j / NST) & 1);
+        PF_T(1, j);
         tc_fence_after();
         const uint32_t kb = skv + st * SM::KV;
 #pragma unroll
@@ -599,7 +607,9 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_kernel(
       for (int j = 0; j < np; ++j) {
         // S_{j+1} overwrites the buffer of P_{j-1}: PV_{j-1} was issued before it
         if (j + 1 < np) issue_s(j + 1);
+        PF_T(2, j);
         mbar_wait(&p_full[j & 1], (j >> 1) & 1);
+        PF_T(3, j);
         tc_fence_after();
         const int st = j % NST;
         const uint32_t vb = skv + st * SM::KV + 16384;
@@ -642,7 +652,11 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_kernel(
         lim = 0;
         self = -1;
       }
+      const bool tw = dbg && (warp == 2 || warp == 6);
+      const int kb = warp == 2 ? 4 : 9;
+      if (tw && lane == 0 && j < 256) dbg[kb * 256 + j] = clock64();
       mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      if (tw && lane == 0 && j < 256) dbg[(kb + 1) * 256 + j] = clock64();
       tc_fence_after();
       uint32_t v[64];
       tmem_ld32(tS + (j & 1) * 64, *reinterpret_cast<uint32_t(*)[32]>(v));
@@ -654,6 +668,7 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_kernel(
         for (int c = 0; c < 64; ++c)
           if (!(c < lim || c == self)) v[c] = __float_as_uint(-INFINITY);
       }
+      if (tw && lane == 0 && j < 256) dbg[(kb + 2) * 256 + j] = clock64();
       float mx = row_max64(v);
       mx *= sl2;
       // lazy rescale: a row moves its reference max only when its running max
@@ -687,8 +702,10 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_kernel(
       // the columns measured slower: the softmax is issue-bound, not MUFU-bound)
       uint32_t pk[32];
       lsum += softmax_pack64(v, sl2, mref, pk);
+      if (tw && lane == 0 && j < 256) dbg[(kb + 3) * 256 + j] = clock64();
       tmem_st32(tS + (j & 1) * 64, pk);  // P over the first 32 columns of its S buffer
       tmem_wait_st();
+      if (tw && lane == 0 && j < 256) dbg[(kb + 4) * 256 + j] = clock64();
       // observe every o_done phase (PV_{j-1}, long complete by now): no phase
       // of the barrier passes unobserved, so a parity wait never aliases
       if (j >= 1) mbar_wait(&o_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
@@ -725,6 +742,8 @@ __global__ __launch_bounds__(64 + 128 * MT, 1) void prefill_attn_kernel(
     tc_fence_after();
     tmem_dealloc(tmem, kTmemCols);
   }
+  if (dbg && threadIdx.x == 0) dbg[14 * 256] = np;
+#undef PF_T
 }
 
 // Persistent variant: one CTA per SM pulls plans (heavy query chunks first)
@@ -1348,6 +1367,7 @@ extern "C" int dhsa_prefill_attn(const void* q, const void* k, const void* v, in
   a.S = S;
   a.counters = counters;
   a.row_stats = reinterpret_cast<float2*>(row_stats);
+  if (const char* e = getenv("DHSA_DEBUG_TIMING")) a.dbg = (unsigned long long*)strtoull(e, nullptr, 0);
   cudaStream_t st = (cudaStream_t)stream;
   // persistent plans pay off when plans are short (per-plan start-up is a
   // large share): measured +7% at budget 1025, -3..-9% at 4097..16385 on the

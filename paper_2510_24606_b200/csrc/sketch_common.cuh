@@ -218,36 +218,51 @@ __device__ void emit_candidates(const SketchArgs& a, const UnitChunks& uc, const
   const int nc = s_ncand;
   unsigned char* row = a.cand + (int64_t)s * a.cand_stride;
   SplitCand* rec = reinterpret_cast<SplitCand*>(row) + 1;
-  for (int i = warp; i < nc && i < a.cand_cap; i += NW) {
-    const int c = list[i];
-    int lo, len;
-    uc.chunk(c, lo, len);
-    double ex;
-    if (c < uc.nc) {
-      const double* crow = a.cent + (int64_t)u * a.c_stride + (int64_t)c * D;
-      double part[G];
+  // a warp re-scores its candidates CB at a time: the CB fp64 centroid rows'
+  // loads are issued together (one memory round trip per batch, not per row)
+  constexpr int CB = 4;
+  const int ncap = nc < a.cand_cap ? nc : a.cand_cap;
+  for (int i0 = warp * CB; i0 < ncap; i0 += NW * CB) {
+    double cv[CB][D / 32];
 #pragma unroll
-      for (int h = 0; h < G; ++h) part[h] = 0.0;
+    for (int b = 0; b < CB; ++b) {
+      const int i = i0 + b;
+      const int c = i < ncap ? list[i] : uc.nc;
+      const double* crow = a.cent + (int64_t)u * a.c_stride + (int64_t)(c < uc.nc ? c : 0) * D;
 #pragma unroll
-      for (int d = lane; d < D; d += 32) {
-        const double cv = crow[d];
-#pragma unroll
-        for (int h = 0; h < G; ++h) part[h] = fma(qd[h][d], cv, part[h]);
-      }
-#pragma unroll
-      for (int h = 0; h < G; ++h) part[h] = warp_sum(part[h]);
-      ex = agg_d<G, AGG>(part + h0, nh);
-    } else {
-      ex = gex;
+      for (int v = 0; v < D / 32; ++v) cv[b][v] = (i < ncap && c < uc.nc) ? crow[lane + 32 * v] : 0.0;
     }
-    if (lane == 0) {
-      SplitCand r;
-      r.score = ex;
-      r.gid = c < uc.nc ? a.chunk_offset + c : a.total_chunks;
-      r.len = len;
-      r.lo = lo;
-      r.pad = 0;
-      rec[i] = r;
+#pragma unroll
+    for (int b = 0; b < CB; ++b) {
+      const int i = i0 + b;
+      if (i >= ncap) break;
+      const int c = list[i];
+      int lo, len;
+      uc.chunk(c, lo, len);
+      double ex;
+      if (c < uc.nc) {
+        double part[G];
+#pragma unroll
+        for (int h = 0; h < G; ++h) part[h] = 0.0;
+#pragma unroll
+        for (int v = 0; v < D / 32; ++v)
+#pragma unroll
+          for (int h = 0; h < G; ++h) part[h] = fma(qd[h][lane + 32 * v], cv[b][v], part[h]);
+#pragma unroll
+        for (int h = 0; h < G; ++h) part[h] = warp_sum(part[h]);
+        ex = agg_d<G, AGG>(part + h0, nh);
+      } else {
+        ex = gex;
+      }
+      if (lane == 0) {
+        SplitCand r;
+        r.score = ex;
+        r.gid = c < uc.nc ? a.chunk_offset + c : a.total_chunks;
+        r.len = len;
+        r.lo = lo;
+        r.pad = 0;
+        rec[i] = r;
+      }
     }
   }
   if (tid == 0) reinterpret_cast<int32_t*>(row)[0] = nc <= a.cand_cap ? nc : -1;

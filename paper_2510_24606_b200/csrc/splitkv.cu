@@ -55,11 +55,14 @@ __global__ __launch_bounds__(kSplitThreads) void split_select_kernel(SplitSelArg
   const int R = (int)(keep - 1);
   for (int it = 0; it < a.items_per_unit; ++it) {
     const int s = u * a.items_per_unit + it;
+    if (tid < a.W)  // every shard's candidate count, loaded together
+      s_off[tid + 1] = __ldcg(reinterpret_cast<const int32_t*>(a.gathered + tid * a.rank_stride +
+                                                               (int64_t)s * a.cand_stride));
+    __syncthreads();
     if (tid == 0) {
       int off = 0, bad = 0;
       for (int r = 0; r < a.W; ++r) {
-        const int nr = *reinterpret_cast<const int32_t*>(a.gathered + r * a.rank_stride +
-                                                         (int64_t)s * a.cand_stride);
+        const int nr = s_off[r + 1];
         s_off[r] = off;
         if (nr < 0 || nr > a.cand_cap) bad = 1;
         else off += nr;
@@ -81,22 +84,36 @@ __global__ __launch_bounds__(kSplitThreads) void split_select_kernel(SplitSelArg
       lo[i] = rec->lo;
     }
     __syncthreads();
-    // takes of this shard's candidates: R minus the tokens ranked before them
+    // takes of this shard's candidates: R minus the tokens ranked before them.
+    // Every thread takes (own candidate, 32-candidate slab) pairs — consecutive
+    // threads different candidates, the same slab (broadcast loads) — and adds
+    // its partial count to the candidate's shared counter: the O(n x mine)
+    // ranking spread over the whole CTA instead of one thread per candidate.
     const int mine0 = s_off[a.rank], mine1 = s_off[a.rank + 1];
-    for (int i = mine0 + tid; i < mine1; i += kSplitThreads) {
-      const uint64_t ki = key[i];
-      const int gi = gid[i];
-      int64_t before = 0;
-      for (int j = 0; j < n; ++j) {
+    const int nm = mine1 - mine0;
+    for (int c = tid; c < nm; c += kSplitThreads) take[c] = 0;  // tokens ranked before
+    __syncthreads();
+    const int nslab = (n + 31) >> 5;
+    for (int w = tid; w < nm * nslab; w += kSplitThreads) {
+      const int c = w % nm, sl = w / nm;
+      const uint64_t ki = key[mine0 + c];
+      const int gi = gid[mine0 + c];
+      const int j1 = min(n, (sl + 1) << 5);
+      int b = 0;
+      for (int j = sl << 5; j < j1; ++j) {
         const uint64_t kj = key[j];
-        if (kj > ki || (kj == ki && gid[j] < gi)) before += len[j];
+        if (kj > ki || (kj == ki && gid[j] < gi)) b += len[j];
       }
-      const int64_t rem = (int64_t)R - before;
-      take[i - mine0] = rem <= 0 ? 0 : (int)(rem < len[i] ? rem : len[i]);
+      if (b) atomicAdd(&take[c], b);
+    }
+    __syncthreads();
+    for (int c = tid; c < nm; c += kSplitThreads) {
+      const int64_t rem = (int64_t)R - take[c];
+      const int li = len[mine0 + c];
+      take[c] = rem <= 0 ? 0 : (int)(rem < li ? rem : li);
     }
     __syncthreads();
     // tiles of <= tile_tokens tokens for the positive takes, then self
-    const int nm = mine1 - mine0;
     const int cpt = (nm + kSplitThreads - 1) / kSplitThreads;
     const int c0 = min(tid * cpt, nm), c1 = min(c0 + cpt, nm);
     int nt_local = 0;
