@@ -25,6 +25,10 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          "--expt-relaxed-constexpr", f"-I{INCLUDE}", f"-I{CSRC}"]
+# extra nvcc flags, e.g. DHSA_NVCC_EXTRA=-DDHSA_SELECT_STAMPS for the select's
+# phase stamps read by tools/step_timeline.py (objects rebuild when it changes)
+EXTRA = os.environ.get("DHSA_NVCC_EXTRA", "").split()
+FLAGS += EXTRA
 
 
 def _deps():
@@ -33,6 +37,9 @@ def _deps():
 
 def _stale(target, sources):
     if not os.path.exists(target):
+        return True
+    stamp = target + ".flags"
+    if not os.path.exists(stamp) or open(stamp).read() != " ".join(EXTRA):
         return True
     t = os.path.getmtime(target)
     return any(os.path.getmtime(s) > t for s in sources)
@@ -46,6 +53,8 @@ def _compile(src, verbose):
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
+    with open(obj + ".flags", "w") as f:
+        f.write(" ".join(EXTRA))
     return obj, r.stderr if verbose else ""
 
 
@@ -64,6 +73,8 @@ def build(verbose: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
+        with open(LIB + ".flags", "w") as f:
+            f.write(" ".join(EXTRA))
     return LIB
 
 

@@ -360,7 +360,12 @@ __global__ __launch_bounds__(NT, NT >= 1024 ? 1 : 3) void sketch_select3_kernel(
       // ---- the chunks kept whole: tiles in chunk order, published early ----
       const int base = s3_emit_whole<kS3WPL>(uc, inbits, a.tile_tokens, out, a.tile_cap, 0,
                                              wlist, kSmallUncertain,
-                                     a.dbg ? a.dbg + kDbgSelectClk + blockIdx.x * 16 : nullptr);
+#ifdef DHSA_SELECT_STAMPS
+                                     a.dbg ? a.dbg + kDbgSelectClk + blockIdx.x * 16 : nullptr
+#else
+                                     nullptr
+#endif
+      );
       __syncwarp();  // the warp's tile stores, before lane 0's (cumulative) release
       if (lane == 0) {
         s_base = base;

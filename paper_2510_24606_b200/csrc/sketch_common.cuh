@@ -74,11 +74,17 @@ struct SketchArgs {
 
 // phase stamps of the select CTAs: clock64 at every point (cheap), the
 // (slow, ~0.5-1 us) %globaltimer only at the start (0) and the end (8)
+// (compiled only with -DDHSA_SELECT_STAMPS: the stamps' code sits between the
+// hot phases of the latency-bound select and costs instruction-cache lines)
+#ifdef DHSA_SELECT_STAMPS
 #define DBG_T(k)                                                           \
   if (a.dbg && threadIdx.x == 0) {                                         \
     if ((k) == 0 || (k) == 8) a.dbg[blockIdx.x * 16 + (k)] = gtimer();     \
     a.dbg[kDbgSelectClk + blockIdx.x * 16 + (k)] = clock64();              \
   }
+#else
+#define DBG_T(k)
+#endif
 
 
 // --------------------------------------------------------------- selection --

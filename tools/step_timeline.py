@@ -2,7 +2,8 @@
 %globaltimer stamps of the sketch stream, select and attention kernels
 (DHSA_DEBUG_TIMING, see common.cuh), printed relative to the earliest sketch
 CTA start.  Usage: python tools/step_timeline.py [B] [context] [split]
-(TL_HQ / TL_HKV set the heads)."""
+(TL_HQ / TL_HKV set the heads).  The select's phase stamps are compiled in only
+with DHSA_NVCC_EXTRA=-DDHSA_SELECT_STAMPS python -m paper_2510_24606_b200.build."""
 import os
 import sys
 
