@@ -421,7 +421,7 @@ def run_gpu(args):
     dtype = getattr(torch, dtn)
     W, S = args.warmup, args.steps
     roll = args.roll_steps  # untimed replays before/after the timed steps (clock sampling)
-    total_steps = W + S + 2 * roll + args.breakdown_steps + args.e2e_steps + 4
+    total_steps = W + S + 2 * roll + args.breakdown_steps + 2 * args.e2e_steps + 8
     dec = SparseDecoder(B, Hq, Hkv, D, L + total_steps, block=blk, top_k=K, dtype=dtype,
                         agg="max", scoring=args.scoring, splits=args.splits)
     gen = torch.Generator(device="cuda")

@@ -268,6 +268,10 @@ class SparseDecoder:
             with torch.cuda.graph(self._pgraph, stream=side):
                 self.launch(q, k, v, self._po, stream=side)
             torch.cuda.current_stream().wait_stream(side)
+        if (qkv.numel() != v1 or qkv.dtype != self.dtype or out.dtype != self.dtype
+                or tuple(out.shape) != (self.B, self.Hq, self.D)):
+            raise ValueError("step_host_packed: qkv must hold [q | k_new | v_new] "
+                             f"({v1} elements of {self.dtype}), out [B, Hq, D] of {self.dtype}")
         self._pin.copy_(qkv.view(-1), non_blocking=True)
         self._pgraph.replay()
         out.copy_(self._po, non_blocking=True)
