@@ -36,11 +36,14 @@
 
 namespace dhsa {
 
-// two shapes: 256 threads x 12 chunks (units of <= 3072 chunks: C2/C3 and
-// every static-grid unit up to 192K tokens) and 1024 threads x 16 chunks
-// (<= 17408 chunks: a 1M-token unit, config C4 on one GPU)
+// shapes: 256 threads x 4 / 9 / 12 chunks (units of <= 1024 / 2304 / 3072
+// chunks: C1/C2, the 128K units of C3 and its rank proxies (2048 prompt
+// chunks + the generated one), every static-grid unit up to 192K tokens) and
+// 1024 threads x 17 chunks (<= 17408 chunks: a 1M-token unit, config C4 on
+// one GPU).  The per-thread element loops are unrolled over the shape's chunk
+// count, so a unit runs the smallest shape that holds it.
 constexpr int kS3Threads = 256;
-constexpr int kS3Per = 12;                           // chunks per thread
+constexpr int kS3PerS = 4, kS3PerM = 9, kS3Per = 12;  // chunks per thread
 constexpr int kS3MaxChunks = kS3Threads * kS3Per;
 constexpr int kS3WideThreads = 1024;
 constexpr int kS3WidePer = 17;  // 17408 >= 16384 prompt chunks + the generated chunk
@@ -201,13 +204,13 @@ template <int D, int G, int AGG, int NT, int kS3Per>
 __global__ __launch_bounds__(NT, NT >= 1024 ? 1 : 3) void sketch_select3_kernel(SketchArgs a) {
   constexpr int NW = NT / 32;
   constexpr int kS3Words = NT * kS3Per / 32;  // bit words per unit
-  constexpr int kS3WPL = kS3Words / 32;       // words per lane of one warp
+  constexpr int kS3WPL = (kS3Words + 31) / 32;  // words per lane of one warp (zero padded)
   __shared__ double qd[G][D];
   __shared__ double s_qn[G], s_gen[G];
   __shared__ uint32_t hist[kHistBins + kHistBins / 32];
   __shared__ float s_mn[NW], s_mx[NW];
   __shared__ int s_win[NW];
-  __shared__ uint32_t inbits[kS3Words], uncbits[kS3Words];
+  __shared__ uint32_t inbits[32 * kS3WPL], uncbits[32 * kS3WPL];
   __shared__ uint64_t ukey[kSmallUncertain];
   __shared__ int32_t ulist[kSmallUncertain], ulen[kSmallUncertain], utake[kSmallUncertain];
   __shared__ int s_nunc, s_base;
@@ -216,6 +219,7 @@ __global__ __launch_bounds__(NT, NT >= 1024 ? 1 : 3) void sketch_select3_kernel(
   const int u = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   pdl_trigger();  // the attention kernel may launch once every select CTA is resident
+  for (int w = kS3Words + tid; w < 32 * kS3WPL; w += NT) inbits[w] = uncbits[w] = 0u;  // padding
   unsigned char* scratch = a.gscratch + (int64_t)u * a.gscratch_stride;
   uint64_t* key64 = reinterpret_cast<uint64_t*>(scratch);
   int32_t* lens = reinterpret_cast<int32_t*>(key64 + a.n_max);

@@ -17,6 +17,8 @@ int launch_select2(const SketchArgs& a, int U, cudaStream_t s, int* rc) {
   cfg.gridDim = dim3((unsigned)U);
   const bool wide = a.n_max > kS3MaxChunks;
   cfg.blockDim = dim3(wide ? kS3WideThreads : kS3Threads);
+  const int per = a.n_max <= kS3Threads * kS3PerS ? kS3PerS
+                  : a.n_max <= kS3Threads * kS3PerM ? kS3PerM : kS3Per;
   cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -26,7 +28,9 @@ int launch_select2(const SketchArgs& a, int U, cudaStream_t s, int* rc) {
   cfg.numAttrs = 1;
   cudaError_t e =
       wide ? cudaLaunchKernelEx(&cfg, sketch_select3_kernel<D, G, AGG, kS3WideThreads, kS3WidePer>, a)
-           : cudaLaunchKernelEx(&cfg, sketch_select3_kernel<D, G, AGG, kS3Threads, kS3Per>, a);
+      : per == kS3PerS ? cudaLaunchKernelEx(&cfg, sketch_select3_kernel<D, G, AGG, kS3Threads, kS3PerS>, a)
+      : per == kS3PerM ? cudaLaunchKernelEx(&cfg, sketch_select3_kernel<D, G, AGG, kS3Threads, kS3PerM>, a)
+                       : cudaLaunchKernelEx(&cfg, sketch_select3_kernel<D, G, AGG, kS3Threads, kS3Per>, a);
   if (e != cudaSuccess) {
     set_error("dhsa_decode_step_bf16(select): %s", cudaGetErrorString(e));
     *rc = DHSA_ECUDA;
