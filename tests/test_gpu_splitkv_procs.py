@@ -139,3 +139,24 @@ def test_bench_c4_two_ranks_gloo():
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["n_gpus"] == 2 and line["config"]["shards"] == 2 and line["value"] > 0
+
+
+def test_bench_c3_heads_sharded_two_ranks_gloo():
+    """bench.py --gpus 2 (C3, heads sharded): self-launched torchrun, two
+    ranks on the one GPU over gloo, each serving 16 q / 4 kv heads of the same
+    32 sequences; rank 0 prints ONE line whose value is the whole job's 32
+    tokens per max-over-ranks step time (strong scaling)."""
+    env = dict(os.environ, DHSA_DIST_BACKEND="gloo")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps",
+                        "3", "--warmup", "3", "--roll-steps", "0", "--breakdown-steps", "2",
+                        "--e2e-steps", "2", "--no-cpu"],
+                       capture_output=True, text=True, timeout=1200, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.strip().splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    line = json.loads(lines[0])
+    cfg = line["config"]
+    assert line["n_gpus"] == 2 and line["scaling"] == "strong"
+    assert cfg["parallelism"] == "heads2" and cfg["global_batch"] == 32
+    assert cfg["rank_shape"] == {"batch": 32, "q_heads": 16, "kv_heads": 4}
+    assert abs(line["value"] - 32 / (line["ms_per_step"] / 1e3)) <= 1e-6 * line["value"]
