@@ -179,7 +179,8 @@ static __device__ __noinline__ void s3_fallback(UnitChunks uc, int n, uint32_t R
                                                 int base, const uint32_t* inbits,
                                                 const uint32_t* uncbits, uint64_t* key64,
                                                 int32_t* lens, int tile_tokens, int32_t* out,
-                                                int64_t tile_cap, int32_t* ntiles_out) {
+                                                int64_t tile_cap, int32_t* ntiles_out,
+                                                int emit) {
   __shared__ WalkShared sh;
   for (int c = threadIdx.x; c < n; c += kS3Threads) {
     const uint32_t bit = 1u << (c & 31);
@@ -194,6 +195,7 @@ static __device__ __noinline__ void s3_fallback(UnitChunks uc, int n, uint32_t R
   uint32_t rrem = R;
   radix_threshold<kS3Threads, uint64_t>(key64, lens, n, R, sh, prefix, mask, rrem);
   walk_takes<kS3Threads, uint64_t>(key64, lens, n, R, prefix, mask, rrem, sh);
+  if (!emit) return;  // split-KV candidate mode: lens[] = every chunk's take
   for (int c = threadIdx.x; c < n; c += kS3Threads)  // the whole chunks were emitted before
     if (key64[c] == ~0ull) lens[c] = 0;
   __syncthreads();
@@ -237,7 +239,9 @@ __global__ __launch_bounds__(NT, NT >= 1024 ? 1 : 3) void sketch_select3_kernel(
   const UnitChunks uc{a.lay, u, nc_u, gl, P_u};
   const int n = uc.nc + (gl >= 1 ? 1 : 0);
   const int wloc = uc.P + gl;  // tokens the walk ranges over (self excluded)
-  const int row = uc.P + g;
+  // the newest token's row: global in split-KV candidate mode (the budget is
+  // the unsharded row's; the local walk keeps every chunk that can take)
+  const int row = a.split ? a.total_prompt + g : uc.P + g;
   const int64_t keep = a.budget < (int64_t)row + 1 ? a.budget : (int64_t)row + 1;
   const uint32_t R = (uint32_t)(keep - 1);
   // sketch units per score unit: 2^-kexp (exact bit construction in the normal range)
@@ -360,7 +364,9 @@ __global__ __launch_bounds__(NT, NT >= 1024 ? 1 : 3) void sketch_select3_kernel(
     }
     __syncthreads();
     DBG_T(9);
-    if (warp == 0) {
+    if (warp == 0 && a.split) {
+      if (lane == 0) s_base = 0;
+    } else if (warp == 0) {
       // ---- the chunks kept whole: tiles in chunk order, published early ----
       const int base = s3_emit_whole<kS3WPL>(uc, inbits, a.tile_tokens, out, a.tile_cap, 0,
                                              wlist, kSmallUncertain,
@@ -438,9 +444,40 @@ __global__ __launch_bounds__(NT, NT >= 1024 ? 1 : 3) void sketch_select3_kernel(
     const int nu = s_nunc;
     const int base = s_base;
     if (a.dbg && tid == 0) a.dbg[blockIdx.x * 16 + 15] = nu;
-    if (nu > kSmallUncertain) {
+    if (a.split) {
+      // split-KV candidates: every chunk with a positive local take, with its
+      // exact fp64 score (emit_candidates), from the takes of every chunk in
+      // global scratch: whole chunks their length, uncertain ones the exact
+      // walk's take (sketch_common.cuh; the generic select's semantics)
+      if (nu > kSmallUncertain) {
+        s3_fallback<NT>(uc, n, R, row, 0, inbits, uncbits, key64, lens, a.tile_tokens, out,
+                        a.tile_cap, a.ntiles + s, 0);
+      } else {
+#pragma unroll
+        for (int e = 0; e < kS3Per; ++e) {
+          const int c = tid + e * NT;
+          if (c < n) lens[c] = (inm & (1u << e)) ? ln[e] : 0;
+        }
+        const int win = warp_sum(lane < NW ? s_win[lane] : 0);
+        const int rp = (int)R - win;
+        for (int i = tid; i < nu; i += NT) {  // rank among the uncertain chunks
+          const uint64_t ki = ukey[i];
+          int before = 0;
+          for (int j = 0; j < nu; ++j) {
+            const uint64_t kj = ukey[j];
+            if (kj > ki || (kj == ki && j < i)) before += ulen[j];  // list = chunk order
+          }
+          const int rem = rp - before;
+          utake[i] = rem <= 0 ? 0 : (rem < ulen[i] ? rem : ulen[i]);
+        }
+        __syncthreads();
+        for (int i = tid; i < nu; i += NT) lens[ulist[i]] = utake[i];
+        __syncthreads();
+      }
+      emit_candidates<D, G, AGG, NT>(a, uc, lens, glist, n, s, qd, h0, nh, gex, u);
+    } else if (nu > kSmallUncertain) {
       s3_fallback<NT>(uc, n, R, row, base, inbits, uncbits, key64, lens, a.tile_tokens, out,
-                  a.tile_cap, a.ntiles + s);
+                  a.tile_cap, a.ntiles + s, 1);
     } else {
       const int win = warp_sum(lane < NW ? s_win[lane] : 0);
       const int rp = (int)R - win;

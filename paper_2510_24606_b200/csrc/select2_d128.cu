@@ -8,9 +8,9 @@ namespace dhsa {
 
 template <int D, int G, int AGG>
 int launch_select2(const SketchArgs& a, int U, cudaStream_t s, int* rc) {
-  // the massive-tie fallback keeps its keys in global scratch; split-KV
-  // candidate mode and longer units use the generic select
-  if (!a.gscratch || a.split || a.n_max > kS3WideMaxChunks) return 0;
+  // the massive-tie fallback keeps its keys (and split-KV candidate mode its
+  // takes) in global scratch; longer units use the generic select
+  if (!a.gscratch || a.n_max > kS3WideMaxChunks) return 0;
   if (const char* e = getenv("DHSA_SELECT2"))
     if (atoi(e) == 0) return 0;
   cudaLaunchConfig_t cfg{};
