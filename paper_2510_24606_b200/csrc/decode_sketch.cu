@@ -703,6 +703,8 @@ static int launch_step(const SketchArgs& a, int U, size_t sel_smem, cudaStream_t
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, score, kTcThreads, ring);
+  // three stream CTAs per SM (sketch_common.cuh: ring depth x CTAs measured)
+  if (per_sm > 3) per_sm = 3;
   if (const char* e = getenv("DHSA_SKETCH_CTAS_PER_SM")) per_sm = atoi(e) > 0 ? atoi(e) : per_sm;
   int64_t grid = (int64_t)sms * (per_sm < 1 ? 1 : per_sm);
   if (grid > a.total_slices) grid = a.total_slices;

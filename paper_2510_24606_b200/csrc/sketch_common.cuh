@@ -20,7 +20,13 @@ constexpr int kHistBins = 1024;  // value-histogram bins of the certified select
 
 constexpr int kTcConsumers = 4;
 constexpr int kTcThreads = (kTcConsumers + 1) * 32;
-constexpr int kTcStages = 4;
+// sketch stream ring: 2 stages x 3 CTAs per SM (measured against 2..6
+// stages x 1..5 CTAs: C3 122.5 vs 123.8 us with 4 x 3, p8 36.6 vs 37.2, p4
+// 48.0 vs 49.4; fewer bytes in flight per SM leave the selects room)
+#ifndef DHSA_SKETCH_STAGES
+#define DHSA_SKETCH_STAGES 2
+#endif
+constexpr int kTcStages = DHSA_SKETCH_STAGES;
 constexpr int kSliceRows = 64;
 
 struct SketchArgs {
