@@ -128,13 +128,25 @@ __global__ __launch_bounds__(kTcThreads) void sketch_score_kernel(
   __syncthreads();
   if (a.dbg && threadIdx.x == 0) a.dbg[kDbgSketch + 2 * blockIdx.x] = gtimer();
   pdl_trigger();  // the select kernel may launch (and run its prologue) right away
-  // contiguous slice range per CTA; (unit, first chunk) advanced incrementally
+  // The slices are streamed in `waves` consecutive parts of the unit range;
+  // in each wave every CTA takes a contiguous slice range, (unit, first
+  // chunk) advanced incrementally.  With 2 waves the first half of the units
+  // is complete at half the stream: their selects run while the stream
+  // finishes the second half (one select CTA fits next to the stream CTAs),
+  // and the attention starts on finished items as soon as the stream's CTAs
+  // leave the SMs.
   const int spu = a.slices_per_unit;
-  const int64_t s_begin = a.total_slices * blockIdx.x / gridDim.x;
-  const int64_t s_end = a.total_slices * (blockIdx.x + 1) / gridDim.x;
-  int u = (int)(s_begin / spu);
-  int c0 = (int)(s_begin - (int64_t)u * spu) * kSliceRows;
-  int nc = a.lay.num_chunks(u);
+  const int nwaves = a.waves > 1 ? a.waves : 1;
+  int64_t s_begin = 0, s_end = 0;
+  int u = 0, c0 = 0, nc = 0;
+  auto wave_range = [&](int w) {
+    const int64_t w0 = a.total_slices * w / nwaves, w1 = a.total_slices * (w + 1) / nwaves;
+    s_begin = w0 + (w1 - w0) * blockIdx.x / gridDim.x;
+    s_end = w0 + (w1 - w0) * (blockIdx.x + 1) / gridDim.x;
+    u = (int)(s_begin / spu);
+    c0 = (int)(s_begin - (int64_t)u * spu) * kSliceRows;
+    nc = s_begin < s_end ? a.lay.num_chunks(u) : 0;
+  };
 
   if (warp == kTcConsumers) {
     if (lane == 0) {
@@ -143,6 +155,8 @@ __global__ __launch_bounds__(kTcThreads) void sketch_score_kernel(
       asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
       if (a.l2_hint) pol = l2_policy_evict_first();
       int it = 0;
+      for (int w = 0; w < nwaves; ++w) {
+      wave_range(w);
       for (int64_t sl = s_begin; sl < s_end; ++sl) {
         if (c0 < nc) {
           const int st = it % kTcStages;
@@ -160,6 +174,7 @@ __global__ __launch_bounds__(kTcThreads) void sketch_score_kernel(
           ++u;
           if (sl + 1 < s_end) nc = a.lay.num_chunks(u);
         }
+      }
       }
     }
     return;
@@ -184,6 +199,8 @@ __global__ __launch_bounds__(kTcThreads) void sketch_score_kernel(
   const int mi = lane >> 3, r8 = lane & 7;
   const int arow = warp * 16 + (mi & 1) * 8 + r8;  // A row addressed by this lane
   int it = 0;
+  for (int w = 0; w < nwaves; ++w) {
+  wave_range(w);
   for (int64_t sl = s_begin; sl < s_end; ++sl, c0 += kSliceRows) {
     if (c0 >= spu * kSliceRows) {
       c0 = 0;
@@ -281,6 +298,7 @@ __global__ __launch_bounds__(kTcThreads) void sketch_score_kernel(
       }
     }
     ++pend_n;  // slices of unit pend_u this warp has scored, published per unit
+  }
   }
   if (a.dbg && threadIdx.x == 0) a.dbg[kDbgSketchPh + 4 * blockIdx.x + 2] = gtimer();
   publish(pend_u, pend_n);
@@ -890,6 +908,12 @@ static int decode_step_impl(
   a.reps = 1;
   if (const char* e = getenv("DHSA_SELECT_REPS")) a.reps = atoi(e) > 0 ? atoi(e) : 1;
   if (const char* e = getenv("DHSA_RELAXED_FLAGS")) a.relaxed = atoi(e);
+  // the sketch stream in 3 waves when there are many units (measured: C3,
+  // 256 units, 122.9 -> 119.3 us/step; p2, 128 units, 72.1 -> 70.0; 4 and 6
+  // waves are slower), in one wave for small batches (C2 / p4, 64 units:
+  // 43.5 vs 44.0 / 48.7 vs 49.0 us with 2 waves)
+  a.waves = U >= 100 ? 3 : 1;
+  if (const char* e = getenv("DHSA_SKETCH_WAVES")) a.waves = atoi(e) > 0 ? atoi(e) : 1;
   const int64_t need = select_scratch_per_unit(layout.max_chunks);
   size_t smem = 0;
   if (scratch) {

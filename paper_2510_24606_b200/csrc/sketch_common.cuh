@@ -65,6 +65,7 @@ struct SketchArgs {
   int l2_hint;              // evict-first L2 policy on the sketch stream
   int reps;                 // (experiment, DHSA_SELECT_REPS) repeated selections
   int relaxed;              // (experiment, DHSA_RELAXED_FLAGS) flag stores without release
+  int waves;                // sketch stream: the unit range in consecutive waves
   unsigned long long* dbg;  // optional per-CTA phase timestamps (DHSA_DEBUG_TIMING)
   // sequence-sharded split-KV mode (dhsa_decode_candidates_bf16): this shard
   // holds global prompt chunks [chunk_offset, chunk_offset + nchunks); the
