@@ -42,6 +42,9 @@ namespace dhsa {
 // 1024 threads x 17 chunks (<= 17408 chunks: a 1M-token unit, config C4 on
 // one GPU).  The per-thread element loops are unrolled over the shape's chunk
 // count, so a unit runs the smallest shape that holds it.
+#ifndef SELECT3_MIN_CTAS
+#define SELECT3_MIN_CTAS 3  // 256-thread shapes: register cap 85 (3) or 64 (4) per thread
+#endif
 constexpr int kS3Threads = 256;
 constexpr int kS3PerS = 4, kS3PerM = 9, kS3Per = 12;  // chunks per thread
 constexpr int kS3MaxChunks = kS3Threads * kS3Per;
@@ -203,7 +206,7 @@ static __device__ __noinline__ void s3_fallback(UnitChunks uc, int n, uint32_t R
 }
 
 template <int D, int G, int AGG, int NT, int kS3Per>
-__global__ __launch_bounds__(NT, NT >= 1024 ? 1 : 3) void sketch_select3_kernel(SketchArgs a) {
+__global__ __launch_bounds__(NT, NT >= 1024 ? 1 : SELECT3_MIN_CTAS) void sketch_select3_kernel(SketchArgs a) {
   constexpr int NW = NT / 32;
   constexpr int kS3Words = NT * kS3Per / 32;  // bit words per unit
   constexpr int kS3WPL = (kS3Words + 31) / 32;  // words per lane of one warp (zero padded)
