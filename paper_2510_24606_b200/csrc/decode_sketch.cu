@@ -140,7 +140,8 @@ __global__ __launch_bounds__(kTcThreads) void sketch_score_kernel(
   int64_t s_begin = 0, s_end = 0;
   int u = 0, c0 = 0, nc = 0;
   auto wave_range = [&](int w) {
-    const int64_t w0 = a.total_slices * w / nwaves, w1 = a.total_slices * (w + 1) / nwaves;
+    const int64_t w0 = w == 0 ? 0 : a.total_slices * a.wave_end[w - 1] / 1000;
+    const int64_t w1 = w == nwaves - 1 ? a.total_slices : a.total_slices * a.wave_end[w] / 1000;
     s_begin = w0 + (w1 - w0) * blockIdx.x / gridDim.x;
     s_end = w0 + (w1 - w0) * (blockIdx.x + 1) / gridDim.x;
     u = (int)(s_begin / spu);
@@ -914,6 +915,16 @@ static int decode_step_impl(
   // 43.5 vs 44.0 / 48.7 vs 49.0 us with 2 waves)
   a.waves = U >= 100 ? 3 : 1;
   if (const char* e = getenv("DHSA_SKETCH_WAVES")) a.waves = atoi(e) > 0 ? atoi(e) : 1;
+  if (a.waves > 4) a.waves = 4;
+  for (int w = 0; w < 4; ++w) a.wave_end[w] = 1000 * (w + 1) / a.waves;  // equal waves
+  if (const char* e = getenv("DHSA_SKETCH_WAVE_ENDS")) {  // e.g. "500,800" (permille)
+    const char* p = e;
+    for (int w = 0; w < a.waves - 1 && *p; ++w) {
+      a.wave_end[w] = atoi(p);
+      while (*p && *p != ',') ++p;
+      if (*p == ',') ++p;
+    }
+  }
   const int64_t need = select_scratch_per_unit(layout.max_chunks);
   size_t smem = 0;
   if (scratch) {

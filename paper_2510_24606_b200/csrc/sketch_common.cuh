@@ -66,6 +66,7 @@ struct SketchArgs {
   int reps;                 // (experiment, DHSA_SELECT_REPS) repeated selections
   int relaxed;              // (experiment, DHSA_RELAXED_FLAGS) flag stores without release
   int waves;                // sketch stream: the unit range in consecutive waves
+  int wave_end[4];          // cumulative wave ends in permille of the slices (waves <= 4)
   unsigned long long* dbg;  // optional per-CTA phase timestamps (DHSA_DEBUG_TIMING)
   // sequence-sharded split-KV mode (dhsa_decode_candidates_bf16): this shard
   // holds global prompt chunks [chunk_offset, chunk_offset + nchunks); the
