@@ -87,8 +87,11 @@ __device__ __forceinline__ void store_row(const StreamArgs& a, int item, int h, 
   }
 }
 
+#ifndef ATTN_MIN_CTAS
+#define ATTN_MIN_CTAS 2  // register cap: 2 -> ~160 per thread, 3 -> 96 (+ spills)
+#endif
 template <int D, int STAGES>
-__global__ __launch_bounds__(192, 2) void attn_stream_kernel(const __grid_constant__ CUtensorMap tmK,
+__global__ __launch_bounds__(192, ATTN_MIN_CTAS) void attn_stream_kernel(const __grid_constant__ CUtensorMap tmK,
                                                           const __grid_constant__ CUtensorMap tmV,
                                                           StreamArgs a) {
   using T = DecodeTile<D>;
