@@ -48,8 +48,12 @@ namespace dhsa {
 constexpr int kS3Threads = 256;
 constexpr int kS3PerS = 4, kS3PerM = 9, kS3Per = 12;  // chunks per thread
 constexpr int kS3MaxChunks = kS3Threads * kS3Per;
-constexpr int kS3WideThreads = 1024;
-constexpr int kS3WidePer = 17;  // 17408 >= 16384 prompt chunks + the generated chunk
+#ifndef S3_WIDE_THREADS
+#define S3_WIDE_THREADS 1024
+#define S3_WIDE_PER 17
+#endif
+constexpr int kS3WideThreads = S3_WIDE_THREADS;
+constexpr int kS3WidePer = S3_WIDE_PER;  // 1024 x 17 = 17408 >= 16384 prompt chunks + the generated one
 constexpr int kS3WideMaxChunks = kS3WideThreads * kS3WidePer;
 
 // tiles of a take of `len` tokens (len <= T in the static grid: one)
@@ -206,8 +210,9 @@ static __device__ __noinline__ void s3_fallback(UnitChunks uc, int n, uint32_t R
 }
 
 template <int D, int G, int AGG, int NT, int kS3Per>
-__global__ __launch_bounds__(NT, NT >= 1024 ? 1 : SELECT3_MIN_CTAS) void sketch_select3_kernel(SketchArgs a) {
+__global__ __launch_bounds__(NT, NT > 256 ? 1 : SELECT3_MIN_CTAS) void sketch_select3_kernel(SketchArgs a) {
   constexpr int NW = NT / 32;
+  static_assert(kS3Per <= 32, "per-thread chunk flags are 32-bit masks");
   constexpr int kS3Words = NT * kS3Per / 32;  // bit words per unit
   constexpr int kS3WPL = (kS3Words + 31) / 32;  // words per lane of one warp (zero padded)
   __shared__ double qd[G][D];
