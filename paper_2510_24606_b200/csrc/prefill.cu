@@ -1370,9 +1370,10 @@ extern "C" int dhsa_prefill_attn(const void* q, const void* k, const void* v, in
   if (const char* e = getenv("DHSA_DEBUG_TIMING")) a.dbg = (unsigned long long*)strtoull(e, nullptr, 0);
   cudaStream_t st = (cudaStream_t)stream;
   // persistent plans pay off when plans are short (per-plan start-up is a
-  // large share): measured +7% at budget 1025, -3..-9% at 4097..16385 on the
-  // static grid; with explicit bounds (many short query tiles) +2% at 4097
-  bool persist = counters != nullptr && (budget <= 1600 || explicit_bounds);
+  // large share): r2 measurement (C5 sweep): +0% at budget 1025, +4.5% at
+  // 2049, +1.8% at 4097, -8% at 8193 / 16385 on the static grid; with
+  // explicit bounds (many short query tiles) +2% at 4097
+  bool persist = counters != nullptr && (budget <= 4200 || explicit_bounds);
   if (const char* e = getenv("DHSA_PREFILL_PERSISTENT")) persist = counters != nullptr && atoi(e) != 0;
   if (persist) {
     if (a.heads_per_cta > 2) return launch_prefill_persist<2, 4>(mq, mk, mv, a, st);
