@@ -25,7 +25,7 @@ namespace dhsa {
 
 constexpr int kStreamMaxSeg = 32;  // record slots per item (bounds the workspace)
 constexpr int kSegTiles = 12;      // tiles per segment (at least)
-constexpr int kSegSmall = 4;       // ... in the tail of the step
+constexpr int kSegSmall = 6;       // ... in the tail of the step (swept 2..16: 6 best at C2, C3, p2, p8)
 
 struct StreamArgs {
   const __nv_bfloat16* q;
@@ -520,7 +520,9 @@ extern "C" int dhsa_attn_stream(const void* q, const void* k_cache, const void* 
   if (const char* e = getenv("DHSA_STREAM_PREFETCH")) a.prefetch = atoi(e);
   a.seg_big = max(seg, (tiles_hint + kStreamMaxSeg - 1) / kStreamMaxSeg);
   a.nseg_big = (tiles_hint + a.seg_big - 1) / a.seg_big;
-  a.seg_small = max(kSegSmall, (tiles_hint + kStreamMaxSeg - 1) / kStreamMaxSeg);
+  int seg_small = kSegSmall;
+  if (const char* e = getenv("DHSA_SEG_SMALL")) seg_small = atoi(e) > 0 ? atoi(e) : seg_small;
+  a.seg_small = max(seg_small, (tiles_hint + kStreamMaxSeg - 1) / kStreamMaxSeg);
   a.nseg_small = (tiles_hint + a.seg_small - 1) / a.seg_small;
   a.out = (__nv_bfloat16*)out;
   a.rec_out = records;

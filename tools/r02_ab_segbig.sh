@@ -1,0 +1,7 @@
+# segment size (DHSA_SEG_TILES, default 12) with the tail segments of 6
+set -u
+for rep in 1 2; do for v in 12 10 14 16; do
+for cfg in "--config C3" "--rank-proxy 2" "--config C2" "--rank-proxy 8"; do
+  r=$(DHSA_SEG_TILES=$v timeout 300 python bench.py $cfg --steps 100 --warmup 10 --no-cpu --e2e-steps 2 --roll-steps 500 --breakdown-steps 2 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['us_per_step'],1))")
+  echo "seg=$v [$cfg] $r"
+done; done; done
