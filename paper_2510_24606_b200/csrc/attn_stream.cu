@@ -426,7 +426,9 @@ static int launch_stream(const CUtensorMap& mk, const CUtensorMap& mv, StreamArg
   // the last ~2 pulls per CTA use small segments
   a.head_items = a.items;
   if (a.nseg_small > a.nseg_big) {
-    const int64_t tail = (2 * C + a.nseg_small - 1) / a.nseg_small;
+    int tp = 2;  // tail pulls per CTA
+    if (const char* e = getenv("DHSA_TAIL_PULLS")) tp = atoi(e) >= 0 ? atoi(e) : tp;
+    const int64_t tail = (tp * C + a.nseg_small - 1) / a.nseg_small;
     a.head_items = (int)(a.items > tail ? a.items - tail : 0);
   }
   const int64_t pulls = (int64_t)a.head_items * a.nseg_big +
