@@ -46,7 +46,12 @@ namespace dhsa {
 #define SELECT3_MIN_CTAS 3  // 256-thread shapes: register cap 85 (3) or 64 (4) per thread
 #endif
 constexpr int kS3Threads = 256;
-constexpr int kS3PerS = 4, kS3PerM = 9, kS3Per = 12;  // chunks per thread
+#ifndef S3_MED_NT
+#define S3_MED_NT 256
+#define S3_MED_PER 9
+#endif
+constexpr int kS3PerS = 4, kS3PerM = S3_MED_PER, kS3Per = 12;  // chunks per thread
+constexpr int kS3ThreadsM = S3_MED_NT;  // threads of the middle shape (C3's 2049-chunk units)
 constexpr int kS3MaxChunks = kS3Threads * kS3Per;
 #ifndef S3_WIDE_THREADS
 #define S3_WIDE_THREADS 1024

@@ -16,9 +16,9 @@ int launch_select2(const SketchArgs& a, int U, cudaStream_t s, int* rc) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)U);
   const bool wide = a.n_max > kS3MaxChunks;
-  cfg.blockDim = dim3(wide ? kS3WideThreads : kS3Threads);
   const int per = a.n_max <= kS3Threads * kS3PerS ? kS3PerS
-                  : a.n_max <= kS3Threads * kS3PerM ? kS3PerM : kS3Per;
+                  : a.n_max <= kS3ThreadsM * kS3PerM ? kS3PerM : kS3Per;
+  cfg.blockDim = dim3(wide ? kS3WideThreads : per == kS3PerM ? kS3ThreadsM : kS3Threads);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -29,7 +29,7 @@ int launch_select2(const SketchArgs& a, int U, cudaStream_t s, int* rc) {
   cudaError_t e =
       wide ? cudaLaunchKernelEx(&cfg, sketch_select3_kernel<D, G, AGG, kS3WideThreads, kS3WidePer>, a)
       : per == kS3PerS ? cudaLaunchKernelEx(&cfg, sketch_select3_kernel<D, G, AGG, kS3Threads, kS3PerS>, a)
-      : per == kS3PerM ? cudaLaunchKernelEx(&cfg, sketch_select3_kernel<D, G, AGG, kS3Threads, kS3PerM>, a)
+      : per == kS3PerM ? cudaLaunchKernelEx(&cfg, sketch_select3_kernel<D, G, AGG, kS3ThreadsM, kS3PerM>, a)
                        : cudaLaunchKernelEx(&cfg, sketch_select3_kernel<D, G, AGG, kS3Threads, kS3Per>, a);
   if (e != cudaSuccess) {
     set_error("dhsa_decode_step_bf16(select): %s", cudaGetErrorString(e));
